@@ -1,0 +1,196 @@
+/*
+ * cora.h -- C ABI of libcora_b200.so: the forward pass of one post-LN transformer
+ * encoder layer over a RAGGED mini-batch on NVIDIA B200 (sm_100a), after
+ * "The CoRa Tensor Compiler: Compilation for Ragged Tensors with Minimal
+ * Padding" (Fegade et al., MLSys 2022, arXiv 2110.10221).
+ *
+ * Problem statement: a ragged tensor is
+ * a dense buffer plus per-sequence lengths/offsets; a ragged operator takes
+ * ragged tensors in and produces a ragged tensor out.  The raggedness (the
+ * lengths) is known before the computation and is shared by every layer
+ * (PAPER.md:333-349, 955-958), so it is turned into offset tables once
+ * (cora_layout_build, the "prelude" of PAPER.md:364-380) and reused.
+ *
+ * Conventions for every entry point
+ *  - Pointers are DEVICE pointers unless the name ends in `_host`.
+ *  - Streams are `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ *    All device work is enqueued asynchronously on that stream; nothing
+ *    synchronises the host except cora_layout_status.
+ *  - Ownership: the caller owns every buffer (inputs, weights, outputs,
+ *    workspaces) and the stream; the library never allocates device memory
+ *    and never frees caller memory ("expects users to
+ *    correctly allocate memory").
+ *  - Packed token layout: sequence b occupies rows [row_off[b], row_off[b]+L_b)
+ *    of a row-major [T, C] matrix, T = sum_b L_b, no padding rows.
+ *    (loop + dimension fusion; fused bound F = sum_o s(o)).
+ *  - bf16 matrices are row-major with 16-byte aligned base pointers and rows.
+ *  - Errors: synchronous argument validation returns CORA_ERR_INVALID (1);
+ *    data errors detected on the device (a negative length, L_b > max_len,
+ *    sum L_b != T) are recorded in the layout's status word and reported by
+ *    cora_layout_status as CORA_ERR_DATA (2) -- in that case the attention
+ *    work list is empty and no kernel reads or writes out of range.  CUDA
+ *    launch errors map to CORA_ERR_CUDA (3), unsupported shapes to
+ *    CORA_ERR_UNSUPPORTED (4).  Mirrors SPEC.md:643 (0 ok, 1 validation,
+ *    2 runtime data error).
+ *  - Zero-length sequences are legal; batch == 0 or T == 0
+ *    is a no-op returning CORA_OK.
+ *  - Determinism: identical inputs give bitwise-identical outputs (no atomics
+ *    in floating-point reductions, no split-K).
+ */
+#ifndef CORA_B200_H_
+#define CORA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t cora_status_t;
+enum {
+  CORA_OK = 0,
+  CORA_ERR_INVALID = 1,
+  CORA_ERR_DATA = 2,
+  CORA_ERR_CUDA = 3,
+  CORA_ERR_UNSUPPORTED = 4,
+  CORA_ERR_NCCL = 5
+};
+
+typedef int32_t cora_dtype_t;
+enum { CORA_DT_BF16 = 0, CORA_DT_F32 = 1 };
+
+typedef int32_t cora_act_t;
+enum { CORA_ACT_NONE = 0, CORA_ACT_RELU = 1, CORA_ACT_GELU_ERF = 2 };
+
+/* Device status word bits (cora_layout_t.status). */
+enum { CORA_STATUS_BAD_LENGTH = 1, CORA_STATUS_SUM_MISMATCH = 2 };
+
+/* Attention work-tile word: bits [0,16) = sequence b, [16,24) = head h,
+ * [24,31) = q-tile qt (rows [128 qt, 128 qt + 128) of sequence b). */
+#define CORA_TILE_ROWS 128
+#define CORA_TILE_B(w) ((w) & 0xFFFF)
+#define CORA_TILE_H(w) (((w) >> 16) & 0xFF)
+#define CORA_TILE_QT(w) (((w) >> 24) & 0x7F)
+
+/*
+ * Offset tables of the ragged storage ("prelude"; A_d arrays
+ * of App. B.1; fusion maps of App. B.2).
+ * Filled by cora_layout_build; device tables live inside the caller's workspace.
+ * Immutable after build; one layout serves every layer of the batch.
+ */
+typedef struct cora_layout {
+  int32_t batch;        /* B */
+  int32_t heads;        /* H */
+  int32_t max_len;      /* upper bound on every L_b (validated on device) */
+  int32_t total_tokens; /* T = sum_b L_b (host-known: the caller packed X) */
+  int32_t n_tiles_max;  /* host bound on the attention work list length */
+  int32_t _pad;
+  const int32_t* lengths; /* [B]   L_b (caller-owned) */
+  int32_t* row_off;       /* [B+1] row_off[b] = sum_{j<b} L_j   (A_1 of [b,i,c], exclusive) */
+  int64_t* attn_off;      /* [B+1] attn_off[b] = sum_{j<b} L_j^2 (A_1 of X[b,i,h,j]) */
+  int32_t* seq_of_tok;    /* [T]   f_fo: fused token index -> sequence b */
+  int32_t* pos_in_seq;    /* [T]   f_fi: fused token index -> position i (f_oif(b,i) = row_off[b]+i) */
+  int32_t* tiles;         /* [n_tiles_max] attention work list, longest first */
+  int32_t* n_tiles;       /* [1]   number of valid entries of `tiles` (0 if status != 0) */
+  int32_t* status;        /* [1]   CORA_STATUS_* bits, 0 = ok */
+} cora_layout_t;
+
+/* Encoder layer parameters (nn.Linear convention W[out, in], bf16; LayerNorm fp32).
+ * w_qkv = [W_q; W_k; W_v] as [3d, d]; head h uses rows [h*d_h, (h+1)*d_h) of each block.
+ * Hyper-parameters of the paper: d_model 512, 8 heads x 64, d_ff 2048. */
+typedef struct cora_encoder_params {
+  int32_t d_model, heads, d_ff;
+  float ln_eps;   /* LayerNorm epsilon (reading c3: 1e-5) */
+  cora_act_t act; /* FF1 activation (reading c1: ReLU) */
+  int32_t _pad;
+  const void *w_qkv, *b_qkv; /* [3d, d] bf16, [3d] bf16 */
+  const void *w_o, *b_o;     /* [d, d], [d] */
+  const void *ln1_g, *ln1_b; /* [d] fp32 */
+  const void *w1, *b1;       /* [d_ff, d], [d_ff] */
+  const void *w2, *b2;       /* [d, d_ff], [d] */
+  const void *ln2_g, *ln2_b; /* [d] fp32 */
+} cora_encoder_params_t;
+
+/* ---------------------------------------------------------------- layout (step a1) */
+
+/* Bytes of workspace cora_layout_build needs for this batch. */
+size_t cora_layout_workspace_bytes(int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len);
+
+/* Build the offset tables on the device (two kernels, no host synchronisation).
+ * lengths: device int32 [batch].  ws: device workspace (>= cora_layout_workspace_bytes,
+ * 256-byte aligned).  out: host struct filled with pointers into ws.
+ * Computes row_off/attn_off (exclusive prefix sums, reading c7), seq_of_tok/pos_in_seq,
+ * the attention tile list ordered by (-ceil(L_b/128), b, h, qt) (reading c15) and the
+ * status word.  Returns CORA_ERR_INVALID on bad arguments (batch < 0, heads < 1 or > 255,
+ * max_len < 0 or > 16383, batch > 65536, null pointers, small workspace). */
+cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, void* ws, size_t ws_bytes, cora_layout_t* out, void* stream);
+
+/* Synchronise `stream` and read the device status word: CORA_OK or CORA_ERR_DATA. */
+cora_status_t cora_layout_status(const cora_layout_t* layout, void* stream);
+
+/* ---------------------------------------------------------------- whole layer */
+
+/* Workspace for cora_encoder_layer_fwd: QKV[T,3d] + O[T,d] + Y1[T,d] + H1[T,d] + F[T,d_ff] + Y2[T,d], bf16. */
+size_t cora_encoder_workspace_bytes(const cora_encoder_params_t* p, int32_t total_tokens);
+
+/* y[T, d] = EncoderLayer(x[T, d]) over the ragged batch described by `layout` (bf16 in/out).
+ * Steps (Table ap_op_times):
+ *   QKV = x W_qkv^T + b_qkv                     (tcgen05 GEMM)
+ *   O   = ragged MHA(QKV)                       (fused tcgen05 attention, longest-first tiles)
+ *   Y1  = O W_o^T + b_o + x                     (GEMM + bias + residual)
+ *   H1  = LN(Y1; ln1)                           (warp-per-row LayerNorm)
+ *   F   = act(H1 W1^T + b1)                     (GEMM + bias + activation)
+ *   Y2  = F W2^T + b2 + H1                      (GEMM + bias + residual)
+ *   y   = LN(Y2; ln2)
+ * x and y must not alias. */
+cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
+                                     void* y, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- op-level entry points */
+
+/* c[m, n] = act(a[m, k] w[n, k]^T + bias[n]) + residual[m, n]  (bf16, fp32 accumulate in TMEM).
+ * bias and residual may be NULL.  Packed "vloop-fused" linear op over T = m tokens
+ * (PAPER.md:598-604, 929-935).  Requires k % 8 == 0, n % 8 == 0, 16-byte aligned pointers. */
+cora_status_t cora_linear_fwd(const void* a, const void* w, const void* bias, const void* residual, void* c,
+                              int32_t m, int32_t n, int32_t k, cora_act_t act, void* stream);
+
+/* o[T, H*d_h] = per sequence, per head softmax(Q_h K_h^T * scale) V_h on qkv[T, 3*H*d_h] (bf16).
+ * Only keys j < L_b of the query's own sequence are attended (no padded rows or columns).
+ * PAPER.md:296-300, 625-633, 2256-2259.  head_dim 64 runs the tcgen05 kernel; other head
+ * dims (<= 128, even) run a SIMT kernel.  Uses layout->tiles / n_tiles / row_off / lengths. */
+cora_status_t cora_ragged_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o, int32_t head_dim,
+                                        float scale, void* stream);
+
+/* Row softmax of the ragged attention matrix X[b, i, h, 0:L_b] stored flat at offset
+ * H*attn_off[b] + (i*H + h)*L_b (App. B.1 lowering); x and y have
+ * H * sum_b L_b^2 elements of dtype dt.  Warp-wide reductions. */
+cora_status_t cora_ragged_softmax_fwd(const cora_layout_t* layout, const void* x, void* y, cora_dtype_t dt,
+                                      void* stream);
+
+/* y[r, :] = LN(x[r, :] (+ residual[r, :]); gamma, beta, eps), biased variance, fp32 math.
+ * x, residual, y of dtype dt; gamma/beta fp32.  residual may be NULL.  cols % 8 == 0. */
+cora_status_t cora_layernorm_fwd(const void* x, const void* residual, const float* gamma, const float* beta, void* y,
+                                 int32_t rows, int32_t cols, float eps, cora_dtype_t dt, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU (host logic) */
+
+/* Contiguous sequence partition over n_ranks minimising the max per-rank cost,
+ * cost(L) = 2L(4d^2 + 2 d d_ff) + 4 d L^2 (the sequence's useful FLOPs; BASELINE.json
+ * north_star "balanced on sum(L_i d + L_i^2) FLOPs"); canonical greedy-left among optimal
+ * plans (reading s1).  seq_begin_host[0..n_ranks]: rank r owns [begin[r], begin[r+1]). */
+cora_status_t cora_shard_plan(const int32_t* lengths_host, int32_t batch, int32_t d_model, int32_t d_ff,
+                              int32_t n_ranks, int32_t* seq_begin_host);
+
+/* ---------------------------------------------------------------- misc */
+const char* cora_status_string(cora_status_t s);
+/* Number of SMs of the current device (for callers sizing their own grids); -1 on error. */
+int32_t cora_device_sm_count(void);
+/* Library build string (arch, version). */
+const char* cora_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CORA_B200_H_ */

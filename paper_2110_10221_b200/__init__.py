@@ -1,0 +1,22 @@
+"""B200-native ragged transformer-encoder layer after CoRa (arXiv 2110.10221).
+
+The product path is libcora_b200.so (C ABI, include/cora.h: hand-written sm_100a kernels);
+this package is its thin ctypes binding.  Importing it loads the library and fails loudly if
+it is missing -- there is no CPU or eager fallback.
+"""
+from . import _lib
+from .api import (  # noqa: F401
+    EncoderLayer,
+    EncoderParams,
+    RaggedLayout,
+    build_info,
+    encoder_layer,
+    layernorm,
+    layout_build,
+    linear,
+    ragged_attention,
+    ragged_softmax,
+    shard_plan,
+)
+
+_lib.lib()  # load now: no silent fallback

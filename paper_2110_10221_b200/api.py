@@ -1,0 +1,219 @@
+"""Thin Python binding over the C ABI (include/cora.h).
+
+PyTorch is used only for device memory (tensors as buffers) and streams; every step of the
+path runs in the kernels of libcora_b200.so.  Function names follow the C entry points.
+There is no CPU or eager fallback: a missing library or a non-CUDA tensor raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as C
+
+_ACT = {"none": C.CORA_ACT_NONE, None: C.CORA_ACT_NONE, "relu": C.CORA_ACT_RELU, "gelu": C.CORA_ACT_GELU_ERF}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("libcora_b200 takes contiguous CUDA tensors only (no CPU fallback)")
+
+
+class RaggedLayout:
+    """Device offset tables of one ragged batch (cora_layout_build).  Reused across layers."""
+
+    def __init__(self, lengths: torch.Tensor, total_tokens: int, heads: int, max_len: int, stream=None):
+        _need_cuda(lengths)
+        if lengths.dtype != torch.int32:
+            raise ValueError("lengths must be int32")
+        self.lengths = lengths
+        B = lengths.numel()
+        nbytes = C.lib().cora_layout_workspace_bytes(B, int(total_tokens), int(heads), int(max_len))
+        if nbytes == 0:
+            raise C.CoraError(C.CORA_ERR_INVALID, "cora_layout_workspace_bytes")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=lengths.device)
+        self.c = C.Layout()
+        C.check(C.lib().cora_layout_build(_ptr(lengths), B, int(total_tokens), int(heads), int(max_len), _ptr(self.ws),
+                                          nbytes, ctypes.byref(self.c), _stream(stream)), "cora_layout_build")
+
+    @property
+    def batch(self):
+        return self.c.batch
+
+    @property
+    def heads(self):
+        return self.c.heads
+
+    @property
+    def total_tokens(self):
+        return self.c.total_tokens
+
+    def status(self, stream=None) -> int:
+        """CORA_OK (0) or CORA_ERR_DATA (2); synchronises the stream."""
+        return C.lib().cora_layout_status(ctypes.byref(self.c), _stream(stream))
+
+    def _view(self, ptr: int, n: int, dtype) -> torch.Tensor:
+        off = ptr - self.ws.data_ptr()
+        size = torch.tensor([], dtype=dtype).element_size()
+        return self.ws[off:off + n * size].view(dtype)
+
+    def tables(self) -> dict:
+        """Views of the device tables (for tests and inspection)."""
+        B, T = self.c.batch, self.c.total_tokens
+        return {
+            "row_off": self._view(self.c.row_off, B + 1, torch.int32),
+            "attn_off": self._view(self.c.attn_off, B + 1, torch.int64),
+            "seq_of_tok": self._view(self.c.seq_of_tok, T, torch.int32),
+            "pos_in_seq": self._view(self.c.pos_in_seq, T, torch.int32),
+            "tiles": self._view(self.c.tiles, self.c.n_tiles_max, torch.int32),
+            "n_tiles": self._view(self.c.n_tiles, 1, torch.int32),
+            "status": self._view(self.c.status, 1, torch.int32),
+        }
+
+
+def layout_build(lengths: torch.Tensor, total_tokens: int, heads: int, max_len: int = 512, stream=None) -> RaggedLayout:
+    return RaggedLayout(lengths, total_tokens, heads, max_len, stream)
+
+
+@dataclass
+class EncoderParams:
+    """Weights of one post-LN encoder layer (nn.Linear [out, in] bf16; LayerNorm fp32), on the GPU."""
+
+    d_model: int
+    heads: int
+    d_ff: int
+    w_qkv: torch.Tensor
+    b_qkv: torch.Tensor
+    w_o: torch.Tensor
+    b_o: torch.Tensor
+    ln1_g: torch.Tensor
+    ln1_b: torch.Tensor
+    w1: torch.Tensor
+    b1: torch.Tensor
+    w2: torch.Tensor
+    b2: torch.Tensor
+    ln2_g: torch.Tensor
+    ln2_b: torch.Tensor
+    ln_eps: float = 1e-5
+    act: str = "relu"
+
+    _names = ("w_qkv", "b_qkv", "w_o", "b_o", "ln1_g", "ln1_b", "w1", "b1", "w2", "b2", "ln2_g", "ln2_b")
+
+    @classmethod
+    def from_host(cls, w, device="cuda", act: str = "relu", ln_eps: float = 1e-5) -> "EncoderParams":
+        """From an object with numpy attributes (e.g. synth.EncoderWeights)."""
+        kw = {}
+        for n in cls._names:
+            dt = torch.float32 if n.startswith("ln") else torch.bfloat16
+            kw[n] = torch.as_tensor(getattr(w, n)).to(dtype=dt).contiguous().to(device)
+        return cls(w.d_model, w.heads, w.d_ff, act=act, ln_eps=ln_eps, **kw)
+
+    def cstruct(self) -> C.EncoderParams:
+        p = C.EncoderParams()
+        p.d_model, p.heads, p.d_ff, p.ln_eps, p.act = self.d_model, self.heads, self.d_ff, self.ln_eps, _ACT[self.act]
+        for n in self._names:
+            t = getattr(self, n)
+            _need_cuda(t)
+            setattr(p, n, t.data_ptr())
+        return p
+
+
+class EncoderLayer:
+    """Reusable encoder-layer call: caches the C parameter struct and the workspace."""
+
+    def __init__(self, params: EncoderParams):
+        self.params = params
+        self.cp = params.cstruct()
+        self.ws = None
+
+    def workspace_bytes(self, total_tokens: int) -> int:
+        return C.lib().cora_encoder_workspace_bytes(ctypes.byref(self.cp), int(total_tokens))
+
+    def __call__(self, x: torch.Tensor, layout: RaggedLayout, out: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+        _need_cuda(x)
+        T = layout.total_tokens
+        if x.dtype != torch.bfloat16 or x.shape != (T, self.params.d_model):
+            raise ValueError("x must be bf16 [T, d_model]")
+        nbytes = self.workspace_bytes(T)
+        if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
+            self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)
+        y = torch.empty_like(x) if out is None else out
+        C.check(C.lib().cora_encoder_layer_fwd(ctypes.byref(self.cp), ctypes.byref(layout.c), _ptr(x), _ptr(y),
+                                               _ptr(self.ws), self.ws.numel(), _stream(stream)),
+                "cora_encoder_layer_fwd")
+        return y
+
+
+def encoder_layer(x: torch.Tensor, layout: RaggedLayout, params: EncoderParams, out=None, stream=None) -> torch.Tensor:
+    return EncoderLayer(params)(x, layout, out=out, stream=stream)
+
+
+def linear(a: torch.Tensor, w: torch.Tensor, bias: Optional[torch.Tensor] = None,
+           residual: Optional[torch.Tensor] = None, act: str = "none", out=None, stream=None) -> torch.Tensor:
+    _need_cuda(a, w, bias, residual)
+    m, k = a.shape
+    n = w.shape[0]
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=a.device) if out is None else out
+    C.check(C.lib().cora_linear_fwd(_ptr(a), _ptr(w), _ptr(bias), _ptr(residual), _ptr(c), m, n, k, _ACT[act],
+                                    _stream(stream)), "cora_linear_fwd")
+    return c
+
+
+def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, scale: Optional[float] = None,
+                     out=None, stream=None) -> torch.Tensor:
+    _need_cuda(qkv)
+    T = layout.total_tokens
+    d = layout.heads * head_dim
+    if qkv.dtype != torch.bfloat16 or qkv.shape != (T, 3 * d):
+        raise ValueError("qkv must be bf16 [T, 3 * heads * head_dim]")
+    o = torch.empty(T, d, dtype=torch.bfloat16, device=qkv.device) if out is None else out
+    s = head_dim ** -0.5 if scale is None else scale
+    C.check(C.lib().cora_ragged_attention_fwd(ctypes.byref(layout.c), _ptr(qkv), _ptr(o), head_dim, s,
+                                              _stream(stream)), "cora_ragged_attention_fwd")
+    return o
+
+
+def ragged_softmax(layout: RaggedLayout, x: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    _need_cuda(x)
+    dt = {torch.bfloat16: C.CORA_DT_BF16, torch.float32: C.CORA_DT_F32}[x.dtype]
+    y = torch.empty_like(x) if out is None else out
+    C.check(C.lib().cora_ragged_softmax_fwd(ctypes.byref(layout.c), _ptr(x), _ptr(y), dt, _stream(stream)),
+            "cora_ragged_softmax_fwd")
+    return y
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, residual: Optional[torch.Tensor] = None,
+              eps: float = 1e-5, out=None, stream=None) -> torch.Tensor:
+    _need_cuda(x, gamma, beta, residual)
+    dt = {torch.bfloat16: C.CORA_DT_BF16, torch.float32: C.CORA_DT_F32}[x.dtype]
+    rows, cols = x.shape
+    y = torch.empty_like(x) if out is None else out
+    C.check(C.lib().cora_layernorm_fwd(_ptr(x), _ptr(residual), _ptr(gamma), _ptr(beta), _ptr(y), rows, cols, eps, dt,
+                                       _stream(stream)), "cora_layernorm_fwd")
+    return y
+
+
+def shard_plan(lengths: Sequence[int], d_model: int, d_ff: int, n_ranks: int) -> list:
+    B = len(lengths)
+    arr = (ctypes.c_int32 * max(B, 1))(*[int(x) for x in lengths])
+    out = (ctypes.c_int32 * (n_ranks + 1))()
+    C.check(C.lib().cora_shard_plan(arr, B, d_model, d_ff, n_ranks, out), "cora_shard_plan")
+    return list(out)
+
+
+def build_info() -> str:
+    return C.lib().cora_build_info().decode()

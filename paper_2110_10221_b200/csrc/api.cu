@@ -1,0 +1,357 @@
+// C ABI of libcora_b200.so (include/cora.h): argument validation, workspace carving, tensor-map
+// creation and the orchestration of the encoder layer.  All arithmetic of the method runs in the
+// kernels of prelude.cu, gemm.cu, attention.cu and elementwise.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "cora_internal.h"
+
+namespace cora {
+
+// ---------------------------------------------------------------- driver entry point for TMA maps
+namespace {
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled_t g_encode = nullptr;
+std::once_flag g_encode_once;
+
+void load_encode() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_encode = reinterpret_cast<PFN_encodeTiled_t>(fn);
+}
+
+int g_sm_count[64] = {0};
+}  // namespace
+
+bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                       uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  std::call_once(g_encode_once, load_encode);
+  if (g_encode == nullptr) return false;
+  if (inner == 0 || outer == 0) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int device_sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (g_sm_count[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sm_count[dev] = n > 0 ? n : 148;
+  }
+  return g_sm_count[dev];
+}
+
+}  // namespace cora
+
+using namespace cora;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+inline cora_status_t cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return CORA_OK;
+  if (e == cudaErrorInvalidValue) return CORA_ERR_UNSUPPORTED;
+  return CORA_ERR_CUDA;
+}
+
+int64_t tiles_bound(int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len) {
+  // sum_b ceil(L_b/128) <= min((T + 127 B) / 128, B * ceil(max_len / 128))
+  const int64_t a = (static_cast<int64_t>(total_tokens) + 127ll * batch) / CORA_TILE_ROWS;
+  const int64_t b = static_cast<int64_t>(batch) * ((max_len + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS);
+  return heads * (a < b ? a : b);
+}
+
+struct LayoutCarve {
+  size_t row_off, attn_off, seq_of_tok, pos_in_seq, tiles, n_tiles, status, total;
+};
+LayoutCarve carve_layout(int32_t batch, int32_t total_tokens, int64_t n_tiles_max) {
+  LayoutCarve c;
+  size_t o = 0;
+  c.attn_off = o;
+  o = align_up(o + sizeof(int64_t) * (batch + 1));
+  c.row_off = o;
+  o = align_up(o + sizeof(int32_t) * (batch + 1));
+  c.seq_of_tok = o;
+  o = align_up(o + sizeof(int32_t) * static_cast<size_t>(total_tokens));
+  c.pos_in_seq = o;
+  o = align_up(o + sizeof(int32_t) * static_cast<size_t>(total_tokens));
+  c.tiles = o;
+  o = align_up(o + sizeof(int32_t) * static_cast<size_t>(n_tiles_max));
+  c.n_tiles = o;
+  o = align_up(o + sizeof(int32_t));
+  c.status = o;
+  o = align_up(o + sizeof(int32_t));
+  c.total = o;
+  return c;
+}
+
+bool layout_args_ok(int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len) {
+  return batch >= 0 && batch <= 65536 && total_tokens >= 0 && heads >= 1 && heads <= 255 && max_len >= 0 &&
+         max_len <= 16383;
+}
+
+struct EncoderCarve {
+  size_t qkv, o, y1, h1, f, y2, total;
+};
+EncoderCarve carve_encoder(const cora_encoder_params_t* p, int32_t T) {
+  EncoderCarve c;
+  const size_t t = static_cast<size_t>(T), d = p->d_model, ff = p->d_ff;
+  size_t o = 0;
+  c.qkv = o;
+  o = align_up(o + 2 * t * 3 * d);
+  c.o = o;
+  o = align_up(o + 2 * t * d);
+  c.y1 = o;
+  o = align_up(o + 2 * t * d);
+  c.h1 = o;
+  o = align_up(o + 2 * t * d);
+  c.f = o;
+  o = align_up(o + 2 * t * ff);
+  c.y2 = o;
+  o = align_up(o + 2 * t * d);
+  c.total = o;
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t cora_layout_workspace_bytes(int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len) {
+  if (!layout_args_ok(batch, total_tokens, heads, max_len)) return 0;
+  return carve_layout(batch, total_tokens, tiles_bound(batch, total_tokens, heads, max_len)).total;
+}
+
+cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, void* ws, size_t ws_bytes, cora_layout_t* out, void* stream) {
+  if (out == nullptr || !layout_args_ok(batch, total_tokens, heads, max_len)) return CORA_ERR_INVALID;
+  if (batch > 0 && lengths == nullptr) return CORA_ERR_INVALID;
+  const int64_t ntm = tiles_bound(batch, total_tokens, heads, max_len);
+  if (ntm > INT32_MAX) return CORA_ERR_INVALID;
+  const LayoutCarve c = carve_layout(batch, total_tokens, ntm);
+  if (ws == nullptr || ws_bytes < c.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
+    return CORA_ERR_INVALID;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  cora_layout_t L;
+  std::memset(&L, 0, sizeof(L));
+  L.batch = batch;
+  L.heads = heads;
+  L.max_len = max_len;
+  L.total_tokens = total_tokens;
+  L.n_tiles_max = static_cast<int32_t>(ntm);
+  L.lengths = lengths;
+  L.row_off = reinterpret_cast<int32_t*>(w + c.row_off);
+  L.attn_off = reinterpret_cast<int64_t*>(w + c.attn_off);
+  L.seq_of_tok = reinterpret_cast<int32_t*>(w + c.seq_of_tok);
+  L.pos_in_seq = reinterpret_cast<int32_t*>(w + c.pos_in_seq);
+  L.tiles = reinterpret_cast<int32_t*>(w + c.tiles);
+  L.n_tiles = reinterpret_cast<int32_t*>(w + c.n_tiles);
+  L.status = reinterpret_cast<int32_t*>(w + c.status);
+  launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream));
+  *out = L;
+  return cuda_status(cudaGetLastError());
+}
+
+cora_status_t cora_layout_status(const cora_layout_t* layout, void* stream) {
+  if (layout == nullptr || layout->status == nullptr) return CORA_ERR_INVALID;
+  int32_t st = 0;
+  cudaError_t e = cudaMemcpyAsync(&st, layout->status, sizeof(st), cudaMemcpyDeviceToHost, as_stream(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(as_stream(stream));
+  if (e != cudaSuccess) return CORA_ERR_CUDA;
+  return st == 0 ? CORA_OK : CORA_ERR_DATA;
+}
+
+size_t cora_encoder_workspace_bytes(const cora_encoder_params_t* p, int32_t total_tokens) {
+  if (p == nullptr || total_tokens < 0) return 0;
+  return carve_encoder(p, total_tokens).total;
+}
+
+cora_status_t cora_linear_fwd(const void* a, const void* w, const void* bias, const void* residual, void* c,
+                              int32_t m, int32_t n, int32_t k, cora_act_t act, void* stream) {
+  if (m < 0 || n <= 0 || k <= 0 || (n % 8) != 0 || (k % 8) != 0) return CORA_ERR_INVALID;
+  if (act < CORA_ACT_NONE || act > CORA_ACT_GELU_ERF) return CORA_ERR_INVALID;
+  if (m == 0) return CORA_OK;
+  if (a == nullptr || w == nullptr || c == nullptr || !aligned16(a) || !aligned16(w) || !aligned16(c))
+    return CORA_ERR_INVALID;
+  if ((bias != nullptr && !aligned16(bias)) || (residual != nullptr && !aligned16(residual))) return CORA_ERR_INVALID;
+  GemmArgs g{a, w, bias, residual, c, m, n, k, act};
+  return cuda_status(launch_gemm(g, as_stream(stream)));
+}
+
+cora_status_t cora_ragged_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o, int32_t head_dim,
+                                        float scale, void* stream) {
+  if (layout == nullptr || head_dim <= 0 || head_dim > 128 || (head_dim % 2) != 0) return CORA_ERR_INVALID;
+  if (layout->total_tokens == 0 || layout->batch == 0) return CORA_OK;
+  if (qkv == nullptr || o == nullptr || !aligned16(qkv) || !aligned16(o)) return CORA_ERR_INVALID;
+  if (((layout->heads * head_dim) % 8) != 0) return CORA_ERR_INVALID;
+  return cuda_status(launch_attention(*layout, qkv, o, head_dim, scale, as_stream(stream)));
+}
+
+cora_status_t cora_ragged_softmax_fwd(const cora_layout_t* layout, const void* x, void* y, cora_dtype_t dt,
+                                      void* stream) {
+  if (layout == nullptr || (dt != CORA_DT_BF16 && dt != CORA_DT_F32)) return CORA_ERR_INVALID;
+  if (layout->total_tokens == 0 || layout->batch == 0) return CORA_OK;
+  if (x == nullptr || y == nullptr) return CORA_ERR_INVALID;
+  return cuda_status(launch_ragged_softmax(*layout, x, y, dt, as_stream(stream)));
+}
+
+cora_status_t cora_layernorm_fwd(const void* x, const void* residual, const float* gamma, const float* beta, void* y,
+                                 int32_t rows, int32_t cols, float eps, cora_dtype_t dt, void* stream) {
+  if (rows < 0 || cols <= 0 || (cols % 8) != 0 || (dt != CORA_DT_BF16 && dt != CORA_DT_F32)) return CORA_ERR_INVALID;
+  if (rows == 0) return CORA_OK;
+  if (x == nullptr || y == nullptr || gamma == nullptr || beta == nullptr || !aligned16(x) || !aligned16(y) ||
+      (residual != nullptr && !aligned16(residual)))
+    return CORA_ERR_INVALID;
+  return cuda_status(launch_layernorm(x, residual, gamma, beta, y, rows, cols, eps, dt, as_stream(stream)));
+}
+
+cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
+                                     void* y, void* ws, size_t ws_bytes, void* stream) {
+  if (p == nullptr || layout == nullptr) return CORA_ERR_INVALID;
+  const int32_t d = p->d_model, H = p->heads, ff = p->d_ff, T = layout->total_tokens;
+  if (d <= 0 || H <= 0 || ff <= 0 || (d % H) != 0 || (d % 8) != 0 || (ff % 8) != 0 || H != layout->heads)
+    return CORA_ERR_INVALID;
+  const int32_t hd = d / H;
+  if (hd > 128 || (hd % 2) != 0) return CORA_ERR_UNSUPPORTED;
+  if (p->act < CORA_ACT_NONE || p->act > CORA_ACT_GELU_ERF) return CORA_ERR_INVALID;
+  if (T == 0 || layout->batch == 0) return CORA_OK;
+  const void* ptrs[] = {p->w_qkv, p->b_qkv, p->w_o, p->b_o, p->ln1_g, p->ln1_b, p->w1, p->b1, p->w2, p->b2,
+                        p->ln2_g, p->ln2_b, x, y, ws};
+  for (const void* q : ptrs)
+    if (q == nullptr || !aligned16(q)) return CORA_ERR_INVALID;
+  if (x == y) return CORA_ERR_INVALID;
+  const EncoderCarve c = carve_encoder(p, T);
+  if (ws_bytes < c.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return CORA_ERR_INVALID;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  void* qkv = w + c.qkv;
+  void* o = w + c.o;
+  void* y1 = w + c.y1;
+  void* h1 = w + c.h1;
+  void* f = w + c.f;
+  void* y2 = w + c.y2;
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e;
+  // a2: QKV = x W_qkv^T + b_qkv
+  if ((e = launch_gemm(GemmArgs{x, p->w_qkv, p->b_qkv, nullptr, qkv, T, 3 * d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
+    return cuda_status(e);
+  // a3: fused ragged attention
+  if ((e = launch_attention(*layout, qkv, o, hd, 1.0f / sqrtf(static_cast<float>(hd)), s)) != cudaSuccess)
+    return cuda_status(e);
+  // a4: Y1 = O W_o^T + b_o + x
+  if ((e = launch_gemm(GemmArgs{o, p->w_o, p->b_o, x, y1, T, d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
+    return cuda_status(e);
+  // a5: H1 = LN1(Y1)
+  if ((e = launch_layernorm(y1, nullptr, static_cast<const float*>(p->ln1_g), static_cast<const float*>(p->ln1_b), h1,
+                            T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
+    return cuda_status(e);
+  // a6: F = act(H1 W1^T + b1)
+  if ((e = launch_gemm(GemmArgs{h1, p->w1, p->b1, nullptr, f, T, ff, d, p->act}, s)) != cudaSuccess)
+    return cuda_status(e);
+  // a7: Y2 = F W2^T + b2 + H1
+  if ((e = launch_gemm(GemmArgs{f, p->w2, p->b2, h1, y2, T, d, ff, CORA_ACT_NONE}, s)) != cudaSuccess)
+    return cuda_status(e);
+  // a8: y = LN2(Y2)
+  if ((e = launch_layernorm(y2, nullptr, static_cast<const float*>(p->ln2_g), static_cast<const float*>(p->ln2_b), y,
+                            T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
+    return cuda_status(e);
+  return CORA_OK;
+}
+
+cora_status_t cora_shard_plan(const int32_t* lengths_host, int32_t batch, int32_t d_model, int32_t d_ff,
+                              int32_t n_ranks, int32_t* seq_begin_host) {
+  if (n_ranks < 1 || batch < 0 || d_model <= 0 || d_ff <= 0 || seq_begin_host == nullptr ||
+      (batch > 0 && lengths_host == nullptr))
+    return CORA_ERR_INVALID;
+  // cost(L) = 2 L (4 d^2 + 2 d d_ff) + 4 d L^2  (useful FLOPs of one sequence)
+  const int64_t per_tok = 2ll * (4ll * d_model * d_model + 2ll * d_model * d_ff);
+  int64_t total = 0, hi_one = 0;
+  for (int32_t b = 0; b < batch; ++b) {
+    const int64_t L = lengths_host[b];
+    if (L < 0) return CORA_ERR_INVALID;
+    const int64_t cst = L * per_tok + 4ll * d_model * L * L;
+    total += cst;
+    if (cst > hi_one) hi_one = cst;
+  }
+  auto cost = [&](int32_t b) {
+    const int64_t L = lengths_host[b];
+    return L * per_tok + 4ll * d_model * L * L;
+  };
+  auto parts_needed = [&](int64_t cap) {
+    int32_t parts = 1;
+    int64_t run = 0;
+    for (int32_t b = 0; b < batch; ++b) {
+      const int64_t cb = cost(b);
+      if (run + cb > cap) {
+        ++parts;
+        run = 0;
+      }
+      run += cb;
+    }
+    return parts;
+  };
+  // smallest capacity C* with a greedy partition into <= n_ranks parts (greedy is optimal for a fixed cap)
+  int64_t lo = hi_one, hi = total > hi_one ? total : hi_one;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (parts_needed(mid) <= n_ranks)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const int64_t cap = lo;
+  int32_t i = 0;
+  seq_begin_host[0] = 0;
+  for (int32_t r = 0; r < n_ranks - 1; ++r) {
+    int64_t run = 0;
+    while (i < batch && run + cost(i) <= cap) run += cost(i++);
+    seq_begin_host[r + 1] = i;
+  }
+  seq_begin_host[n_ranks] = batch;
+  return CORA_OK;
+}
+
+const char* cora_status_string(cora_status_t s) {
+  switch (s) {
+    case CORA_OK:
+      return "ok";
+    case CORA_ERR_INVALID:
+      return "invalid argument";
+    case CORA_ERR_DATA:
+      return "data error (bad lengths or sum(L) != T)";
+    case CORA_ERR_CUDA:
+      return "CUDA error";
+    case CORA_ERR_UNSUPPORTED:
+      return "unsupported shape";
+    case CORA_ERR_NCCL:
+      return "NCCL error";
+    default:
+      return "unknown status";
+  }
+}
+
+int32_t cora_device_sm_count(void) { return device_sm_count(); }
+
+const char* cora_build_info(void) { return "libcora_b200 sm_100a tcgen05/TMA; CUDA " CORA_CUDA_VERSION_STR; }
+
+}  // extern "C"

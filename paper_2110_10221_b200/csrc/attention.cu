@@ -1,0 +1,400 @@
+// Step a3: fused ragged multi-head attention (QK^T -> softmax -> .V) per (sequence, head, q-tile).
+//
+// Paper: the SDPA sub-module is where CoRa beats FasterTransformer, because
+// it computes only (partially padded) per-sequence L_b x L_b score blocks instead of a fully
+// padded B x L_max x L_max tensor; thread blocks are ordered
+// longest-sequence-first.  CoRa runs QK^T, softmax and AttnV as three
+// kernels with the ragged score tensor X[b,i,h,j] in HBM.
+//
+// sm_100a design: nothing of S or P touches HBM.  A persistent CTA walks the
+// longest-first tile list built by the prelude (static stride over the list).  For one work
+// tile (b, h, qt): Q = 128 query rows of sequence b, head h; K_j / V_j = 128-key tiles,
+// j < ceil(L_b / 128).
+//   warp 0     : TMA producer (Q, K ring of 2, V) from QKV[T, 3d] with 128x64 SWIZZLE_128B boxes
+//   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer
+//                  S_j = Q K_j^T  (M128 N128 K64, fp32 in TMEM cols [0,128))
+//                  O_j = P_j V_j  (M128 N64 K128, V as an MN-major operand, TMEM cols [128,192))
+//   warps 2..5 : softmax / correction / epilogue, one query row per thread (TMEM lane = row):
+//                  online softmax in the exp2 domain, masking keys >= L_b with -inf
+//                  (reading c18), P_j -> bf16 -> swizzled smem (A operand of the PV MMA),
+//                  o = o * alpha + O_j in registers, o / l -> bf16 -> predicated row stores
+//                  (rows >= L_b belong to the next sequence and are never written).
+// Rows of a 128-row TMA box that lie past the sequence end are real rows of the next
+// sequence (finite) or TMA zero-fill past T: their keys are masked and their queries discarded.
+// Two CTAs per SM (96 KB smem, 256 TMEM columns each) overlap one CTA's softmax with the other's MMAs.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "cora_internal.h"
+#include "ptx.cuh"
+
+namespace cora {
+namespace {
+
+constexpr int HD = 64;        // head dim (one SWIZZLE_128B row)
+constexpr int TQ = 128;       // query rows per work tile
+constexpr int TK = 128;       // keys per KV tile
+constexpr int KSTAGES = 2;    // K ring depth
+constexpr int kThreads = 192;
+constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
+
+struct AttnSmem {
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + kTileBytes;
+  static constexpr int kOffV = kOffK + KSTAGES * kTileBytes;
+  static constexpr int kOffP = kOffV + kTileBytes;          // two 128x64 sub-tiles (keys 0-63, 64-127)
+  static constexpr int kOffBar = kOffP + 2 * kTileBytes;
+  // q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty, s_full, s_empty, p_full, o_full, o_empty
+  static constexpr int kNumBars = 2 + 2 * KSTAGES + 2 + 2 + 1 + 2;
+  static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
+  static constexpr int kAlloc = kBytes + 1024;
+};
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemS = 0, kTmemO = 128;
+
+__device__ __forceinline__ void decode_tile(int32_t w, int& b, int& h, int& qt) {
+  b = w & 0xFFFF;
+  h = (w >> 16) & 0xFF;
+  qt = (w >> 24) & 0x7F;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
+                         const int32_t* __restrict__ n_tiles_ptr, const int32_t* __restrict__ lengths,
+                         const int32_t* __restrict__ row_off, __nv_bfloat16* __restrict__ out, int32_t d_model,
+                         float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::kOffBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + KSTAGES;
+  uint64_t* v_full = k_empty + KSTAGES;
+  uint64_t* v_empty = v_full + 1;
+  uint64_t* s_full = v_empty + 1;
+  uint64_t* s_empty = s_full + 1;
+  uint64_t* p_full = s_empty + 1;
+  uint64_t* o_full = p_full + 1;
+  uint64_t* o_empty = o_full + 1;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + AttnSmem::kNumBars);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int n_tiles = *n_tiles_ptr;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < KSTAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(s_empty, 4);
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_ptr);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t q_ph = 0, v_ph = 0, k_ph = 0;
+      int ks = 0;
+      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+        int b, h, qt;
+        decode_tile(tiles[idx], b, h, qt);
+        const int L = lengths[b], r0 = row_off[b];
+        const int nkv = (L + TK - 1) / TK;
+        mbar_wait(q_empty, q_ph ^ 1);
+        q_ph ^= 1;
+        mbar_arrive_expect_tx(q_full, kTileBytes);
+        tma_load_2d(smem + AttnSmem::kOffQ, &tm_qkv, q_full, h * HD, r0 + qt * TQ);
+        for (int j = 0; j < nkv; ++j) {
+          mbar_wait(&k_empty[ks], k_ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
+          tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + h * HD, r0 + j * TK);
+          if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+          mbar_wait(v_empty, v_ph ^ 1);
+          v_ph ^= 1;
+          mbar_arrive_expect_tx(v_full, kTileBytes);
+          tma_load_2d(smem + AttnSmem::kOffV, &tm_qkv, v_full, 2 * d_model + h * HD, r0 + j * TK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK);
+      constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HD, /*b_mn_major=*/true);
+      const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ);
+      const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV);
+      const uint32_t p_addr = smem_u32(smem + AttnSmem::kOffP);
+      uint32_t q_ph = 0, v_ph = 0, k_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
+      int ks = 0;
+      auto issue_s = [&](int j, int nkv) {
+        mbar_wait(&k_full[ks], k_ph);
+        mbar_wait(s_empty, s_ph ^ 1);
+        s_ph ^= 1;
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
+                       make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
+        umma_commit(&k_empty[ks]);
+        umma_commit(s_full);
+        if (j == nkv - 1) umma_commit(q_empty);
+        if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+      };
+      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+        int b, h, qt;
+        decode_tile(tiles[idx], b, h, qt);
+        const int L = lengths[b];
+        const int nkv = (L + TK - 1) / TK;
+        mbar_wait(q_full, q_ph);
+        q_ph ^= 1;
+        issue_s(0, nkv);
+        for (int j = 0; j < nkv; ++j) {
+          if (j + 1 < nkv) issue_s(j + 1, nkv);
+          mbar_wait(p_full, p_ph);
+          p_ph ^= 1;
+          mbar_wait(v_full, v_ph);
+          v_ph ^= 1;
+          mbar_wait(o_empty, o_ph ^ 1);
+          o_ph ^= 1;
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k) {
+            // A = P (K-major, keys 64*(k/4).. in sub-tile k/4), B = V (MN-major: 16 key rows per step)
+            const uint64_t pd = make_sdesc_sw128(p_addr + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
+            const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
+            umma_bf16_ss(tmem_base + kTmemO, pd, vd, idesc_o, k != 0);
+          }
+          umma_commit(v_empty);
+          umma_commit(o_full);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / correction / epilogue
+    const uint32_t qd = warp & 3;  // TMEM lane quadrant
+    const int i = qd * 32 + lane;  // query row within the tile
+    const uint32_t t_lane = (qd * 32) << 16;
+    const uint32_t p_base = smem_u32(smem + AttnSmem::kOffP);
+    uint32_t s_ph = 0, o_ph = 0;
+    for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+      int b, h, qt;
+      decode_tile(tiles[idx], b, h, qt);
+      const int L = lengths[b], r0 = row_off[b];
+      const int nkv = (L + TK - 1) / TK;
+      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+      float o[HD];
+#pragma unroll
+      for (int c = 0; c < HD; ++c) o[c] = 0.f;
+
+      auto accumulate_o = [&](float alpha) {
+        mbar_wait(o_full, o_ph);
+        o_ph ^= 1;
+        tc_fence_after();
+        uint32_t r[32];
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + half * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[half * 32 + c] = o[half * 32 + c] * alpha + __uint_as_float(r[c]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty);
+      };
+
+      for (int j = 0; j < nkv; ++j) {
+        const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
+        mbar_wait(s_full, s_ph);
+        s_ph ^= 1;
+        tc_fence_after();
+        // pass 1: row max over the valid keys
+        float mx = -INFINITY;
+#pragma unroll
+        for (int cb = 0; cb < TK / 32; ++cb) {
+          uint32_t r[32];
+          CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (cb * 32 + c < valid) mx = fmaxf(mx, __uint_as_float(r[c]));
+        }
+        const float m_new = fmaxf(m, mx * scale_log2);
+        const float alpha = ex2_approx(m - m_new);
+        m = m_new;
+        // P_{j-1} must be consumed (and O_{j-1} folded in) before P_j overwrites the smem tile
+        if (j > 0) accumulate_o(alpha_prev);
+        // pass 2: p = exp2(s*scale_log2 - m), row sum, bf16 P -> swizzled smem
+        float rs = 0.f;
+#pragma unroll
+        for (int cb = 0; cb < TK / 32; ++cb) {
+          uint32_t r[32];
+          CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, r);
+          tmem_ld_wait();
+          float p[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            p[c] = (cb * 32 + c < valid) ? ex2_approx(__uint_as_float(r[c]) * scale_log2 - m) : 0.f;
+            rs += p[c];
+          }
+          const uint32_t sub = p_base + (cb >> 1) * kTileBytes;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t ch = (cb & 1) * 4 + g;
+            st_shared_v4(sub + sw128_offset(i, ch), pack_bf16x2(p[g * 8 + 0], p[g * 8 + 1]),
+                         pack_bf16x2(p[g * 8 + 2], p[g * 8 + 3]), pack_bf16x2(p[g * 8 + 4], p[g * 8 + 5]),
+                         pack_bf16x2(p[g * 8 + 6], p[g * 8 + 7]));
+          }
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(s_empty);
+          mbar_arrive(p_full);
+        }
+        l = l * alpha + rs;
+        alpha_prev = alpha;
+      }
+      accumulate_o(alpha_prev);
+      // epilogue: normalise and store the valid query rows of this tile
+      const int qrow = qt * TQ + i;
+      if (qrow < L) {
+        const float inv = 1.f / l;
+        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(r0 + qrow) * d_model + h * HD);
+#pragma unroll
+        for (int g = 0; g < HD / 8; ++g)
+          dst[g] = make_uint4(pack_bf16x2(o[g * 8 + 0] * inv, o[g * 8 + 1] * inv),
+                              pack_bf16x2(o[g * 8 + 2] * inv, o[g * 8 + 3] * inv),
+                              pack_bf16x2(o[g * 8 + 4] * inv, o[g * 8 + 5] * inv),
+                              pack_bf16x2(o[g * 8 + 6] * inv, o[g * 8 + 7] * inv));
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- SIMT kernel for other head dims
+// One warp per (token, head): online softmax over the keys of the token's own sequence, 32 keys
+// at a time (lane = key), probabilities broadcast with shuffles, lane owns dims lane + 32k.
+// Serves head_dim != 64 (e.g. the tiny C1 configuration, d_h = 8) where a 128x64 UMMA tile does
+// not apply.
+template <int DPL>  // dims per lane: head_dim <= 32 * DPL
+__global__ void __launch_bounds__(256) attention_simt_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                             __nv_bfloat16* __restrict__ out,
+                                                             const int32_t* __restrict__ lengths,
+                                                             const int32_t* __restrict__ row_off,
+                                                             const int32_t* __restrict__ seq_of_tok, int32_t T,
+                                                             int32_t heads, int32_t hd, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wg >= static_cast<int64_t>(T) * heads) return;
+  const int t = static_cast<int>(wg / heads), h = static_cast<int>(wg % heads);
+  const int b = seq_of_tok[t];
+  if (b < 0) return;
+  const int L = lengths[b], r0 = row_off[b];
+  const int d = heads * hd, ld = 3 * d;
+  const __nv_bfloat16* q = qkv + static_cast<size_t>(t) * ld + h * hd;
+  float m = -INFINITY, l = 0.f, o[DPL];
+#pragma unroll
+  for (int k = 0; k < DPL; ++k) o[k] = 0.f;
+  for (int j0 = 0; j0 < L; j0 += 32) {
+    const int j = j0 + lane;
+    float s = -INFINITY;
+    if (j < L) {
+      const __nv_bfloat16* kr = qkv + static_cast<size_t>(r0 + j) * ld + d + h * hd;
+      float acc = 0.f;
+      for (int c = 0; c < hd; ++c) acc += __bfloat162float(q[c]) * __bfloat162float(kr[c]);
+      s = acc * scale;
+    }
+    float mx = s;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const float m_new = fmaxf(m, mx);
+    const float alpha = __expf(m - m_new);
+    const float p = j < L ? __expf(s - m_new) : 0.f;
+    float ps = p;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+    l = l * alpha + ps;
+    m = m_new;
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) o[k] *= alpha;
+    const int nk = min(32, L - j0);
+    for (int jj = 0; jj < nk; ++jj) {
+      const float pj = __shfl_sync(0xffffffffu, p, jj);
+      const __nv_bfloat16* vr = qkv + static_cast<size_t>(r0 + j0 + jj) * ld + 2 * d + h * hd;
+#pragma unroll
+      for (int k = 0; k < DPL; ++k) {
+        const int c = lane + 32 * k;
+        if (c < hd) o[k] += pj * __bfloat162float(vr[c]);
+      }
+    }
+  }
+  __nv_bfloat16* dst = out + static_cast<size_t>(t) * d + h * hd;
+#pragma unroll
+  for (int k = 0; k < DPL; ++k) {
+    const int c = lane + 32 * k;
+    if (c < hd) dst[c] = __float2bfloat16_rn(o[k] / l);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
+                             cudaStream_t stream) {
+  if (L.total_tokens == 0 || L.batch == 0) return cudaSuccess;
+  const int32_t d = L.heads * head_dim;
+  if (head_dim == HD) {
+    CUtensorMap tm;
+    if (!make_tmap_2d_bf16(&tm, qkv, 3ull * d, L.total_tokens, 3ull * d * 2, HD, TQ, true))
+      return cudaErrorInvalidValue;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e =
+          cudaFuncSetAttribute(attention_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem::kAlloc);
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    const int max_grid = 2 * device_sm_count();
+    const int grid = L.n_tiles_max < max_grid ? L.n_tiles_max : max_grid;
+    if (grid == 0) return cudaSuccess;
+    const float scale_log2 = scale * 1.4426950408889634f;
+    attention_fwd_kernel<<<grid, kThreads, AttnSmem::kAlloc, stream>>>(
+        tm, L.tiles, L.n_tiles, L.lengths, L.row_off, static_cast<__nv_bfloat16*>(o), d, scale_log2);
+    return cudaGetLastError();
+  }
+  const int64_t warps = static_cast<int64_t>(L.total_tokens) * L.heads;
+  const dim3 block(256), grid(static_cast<unsigned>((warps + 7) / 8));
+  auto q = static_cast<const __nv_bfloat16*>(qkv);
+  auto out = static_cast<__nv_bfloat16*>(o);
+  if (head_dim <= 32)
+    attention_simt_kernel<1><<<grid, block, 0, stream>>>(q, out, L.lengths, L.row_off, L.seq_of_tok,
+                                                         L.total_tokens, L.heads, head_dim, scale);
+  else
+    attention_simt_kernel<4><<<grid, block, 0, stream>>>(q, out, L.lengths, L.row_off, L.seq_of_tok,
+                                                         L.total_tokens, L.heads, head_dim, scale);
+  return cudaGetLastError();
+}
+
+}  // namespace cora

@@ -1,0 +1,44 @@
+// Internal launcher declarations shared by the kernel translation units and api.cu.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/cora.h"
+
+namespace cora {
+
+constexpr int kAttnHeadDim = 64;  // head_dim of the tcgen05 attention kernel
+
+void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
+                         const cora_layout_t& L, cudaStream_t stream);
+
+// GEMM: C[m,n] = act(A[m,k] B[n,k]^T + bias) + residual.  Tensor maps are built by the caller.
+struct GemmArgs {
+  const void* a;
+  const void* b;
+  const void* bias;
+  const void* residual;
+  void* c;
+  int32_t m, n, k;
+  int32_t act;
+};
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
+
+cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
+                             cudaStream_t stream);
+
+cudaError_t launch_layernorm(const void* x, const void* residual, const float* gamma, const float* beta, void* y,
+                             int32_t rows, int32_t cols, float eps, cora_dtype_t dt, cudaStream_t stream);
+
+cudaError_t launch_ragged_softmax(const cora_layout_t& L, const void* x, void* y, cora_dtype_t dt,
+                                  cudaStream_t stream);
+
+// Tensor-map creation through the driver entry point (no -lcuda link dependency).
+bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                       uint32_t box_inner, uint32_t box_outer, bool swizzle128);
+
+int device_sm_count();
+
+}  // namespace cora

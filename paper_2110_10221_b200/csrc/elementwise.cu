@@ -1,0 +1,289 @@
+// Steps a5/a8 (LayerNorm) and a3' (standalone ragged softmax): HBM-bound warp-per-row kernels.
+//
+// Both use warp-wide shuffle reductions instead of block-wide ones, the schedule CoRa found
+// faster than FasterTransformer's block reductions (App. D.6): no
+// __syncthreads, and the reduction never touches padding because rows are read at their
+// exact ragged extent.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "cora_internal.h"
+
+namespace cora {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T>
+struct Vec;  // 16-byte vectors
+template <>
+struct Vec<float> {
+  static constexpr int E = 4;
+  __device__ static void load(const float* p, float* v) {
+    float4 q = *reinterpret_cast<const float4*>(p);
+    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+  }
+  __device__ static void store(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int E = 8;
+  __device__ static void load(const __nv_bfloat16* p, float* v) {
+    uint4 q = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+  __device__ static void store(__nv_bfloat16* p, const float* v) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+// One warp per row; NV 16-byte vectors per lane held in registers (cols <= 32 * NV * E).
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ res,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta, T* __restrict__ y,
+                                                        int32_t rows, int32_t cols, float eps) {
+  constexpr int E = Vec<T>::E;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols / E;
+  const size_t rbase = static_cast<size_t>(row) * cols;
+  float v[NV][E];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int vi = lane + 32 * j;
+    if (vi < nvec) {
+      Vec<T>::load(x + rbase + vi * E, v[j]);
+      if (res != nullptr) {
+        float r[E];
+        Vec<T>::load(res + rbase + vi * E, r);
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[j][e] += r[e];
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) s += v[j][e];
+    }
+  }
+  const float mean = warp_sum(s) / cols;
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    if (lane + 32 * j < nvec) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float dlt = v[j][e] - mean;
+        q += dlt * dlt;
+      }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / cols + eps);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int vi = lane + 32 * j;
+    if (vi < nvec) {
+      float o[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int c = vi * E + e;
+        o[e] = (v[j][e] - mean) * rstd * __ldg(gamma + c) + __ldg(beta + c);
+      }
+      Vec<T>::store(y + rbase + vi * E, o);
+    }
+  }
+}
+
+// Rows wider than the register budget: three passes over global memory (L1/L2 hits after the first).
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_wide_kernel(const T* __restrict__ x, const T* __restrict__ res,
+                                                             const float* __restrict__ gamma,
+                                                             const float* __restrict__ beta, T* __restrict__ y,
+                                                             int32_t rows, int32_t cols, float eps) {
+  constexpr int E = Vec<T>::E;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols / E;
+  const size_t rbase = static_cast<size_t>(row) * cols;
+  auto load = [&](int vi, float* v) {
+    Vec<T>::load(x + rbase + vi * E, v);
+    if (res != nullptr) {
+      float r[E];
+      Vec<T>::load(res + rbase + vi * E, r);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] += r[e];
+    }
+  };
+  float s = 0.f;
+  for (int vi = lane; vi < nvec; vi += 32) {
+    float v[E];
+    load(vi, v);
+#pragma unroll
+    for (int e = 0; e < E; ++e) s += v[e];
+  }
+  const float mean = warp_sum(s) / cols;
+  float q = 0.f;
+  for (int vi = lane; vi < nvec; vi += 32) {
+    float v[E];
+    load(vi, v);
+#pragma unroll
+    for (int e = 0; e < E; ++e) q += (v[e] - mean) * (v[e] - mean);
+  }
+  const float rstd = rsqrtf(warp_sum(q) / cols + eps);
+  for (int vi = lane; vi < nvec; vi += 32) {
+    float v[E], o[E];
+    load(vi, v);
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = (v[e] - mean) * rstd * gamma[vi * E + e] + beta[vi * E + e];
+    Vec<T>::store(y + rbase + vi * E, o);
+  }
+}
+
+template <typename T>
+cudaError_t dispatch_layernorm(const void* x, const void* res, const float* g, const float* b, void* y, int32_t rows,
+                               int32_t cols, float eps, cudaStream_t s) {
+  constexpr int E = Vec<T>::E;
+  const int per_lane = (cols / E + 31) / 32;
+  const dim3 block(256), grid((rows + 7) / 8);
+  auto X = static_cast<const T*>(x);
+  auto R = static_cast<const T*>(res);
+  auto Y = static_cast<T*>(y);
+  if (per_lane <= 1)
+    layernorm_kernel<T, 1><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+  else if (per_lane <= 2)
+    layernorm_kernel<T, 2><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+  else if (per_lane <= 4)
+    layernorm_kernel<T, 4><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+  else
+    layernorm_wide_kernel<T><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- ragged softmax (a3')
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p);
+template <>
+__device__ __forceinline__ float ld_f<float>(const float* p) {
+  return __ldg(p);
+}
+template <>
+__device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+template <typename T>
+__device__ __forceinline__ void st_f(T* p, float v);
+template <>
+__device__ __forceinline__ void st_f<float>(float* p, float v) {
+  *p = v;
+}
+template <>
+__device__ __forceinline__ void st_f<__nv_bfloat16>(__nv_bfloat16* p, float v) {
+  *p = __float2bfloat16_rn(v);
+}
+
+// One warp per row (b, i, h) of X[b, i, h, 0:L_b].  Row r = t*H + h with t the fused token index,
+// b = f_fo(t), i = f_fi(t) (App. B.2 maps); the row starts at H*attn_off[b] + (i*H + h)*L_b
+// (App. B.1 lowering).  Consecutive rows are contiguous, so a block streams a contiguous range.
+template <typename T, int MAXE>
+__global__ void __launch_bounds__(256) ragged_softmax_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                             const int32_t* __restrict__ lengths,
+                                                             const int64_t* __restrict__ attn_off,
+                                                             const int32_t* __restrict__ seq_of_tok,
+                                                             const int32_t* __restrict__ pos_in_seq, int32_t heads,
+                                                             int64_t n_rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_rows) return;
+  const int32_t t = static_cast<int32_t>(r / heads), h = static_cast<int32_t>(r % heads);
+  const int32_t b = seq_of_tok[t];
+  if (b < 0) return;  // layout status != 0
+  const int32_t i = pos_in_seq[t];
+  const int32_t L = lengths[b];
+  const int64_t base = heads * attn_off[b] + static_cast<int64_t>(i * heads + h) * L;
+  const T* xr = x + base;
+  T* yr = y + base;
+  if (L <= 32 * MAXE) {
+    float v[MAXE];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < MAXE; ++k) {
+      const int j = lane + 32 * k;
+      v[k] = j < L ? ld_f(xr + j) : -INFINITY;
+      m = fmaxf(m, v[k]);
+    }
+    m = warp_max(m);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXE; ++k) {
+      const int j = lane + 32 * k;
+      v[k] = j < L ? expf(v[k] - m) : 0.f;
+      s += v[k];
+    }
+    const float inv = 1.0f / warp_sum(s);
+#pragma unroll
+    for (int k = 0; k < MAXE; ++k) {
+      const int j = lane + 32 * k;
+      if (j < L) st_f(yr + j, v[k] * inv);
+    }
+  } else {
+    float m = -INFINITY;
+    for (int j = lane; j < L; j += 32) m = fmaxf(m, ld_f(xr + j));
+    m = warp_max(m);
+    float s = 0.f;
+    for (int j = lane; j < L; j += 32) s += expf(ld_f(xr + j) - m);
+    const float inv = 1.0f / warp_sum(s);
+    for (int j = lane; j < L; j += 32) st_f(yr + j, expf(ld_f(xr + j) - m) * inv);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_layernorm(const void* x, const void* residual, const float* gamma, const float* beta, void* y,
+                             int32_t rows, int32_t cols, float eps, cora_dtype_t dt, cudaStream_t stream) {
+  if (rows == 0) return cudaSuccess;
+  if (dt == CORA_DT_BF16)
+    return dispatch_layernorm<__nv_bfloat16>(x, residual, gamma, beta, y, rows, cols, eps, stream);
+  return dispatch_layernorm<float>(x, residual, gamma, beta, y, rows, cols, eps, stream);
+}
+
+cudaError_t launch_ragged_softmax(const cora_layout_t& L, const void* x, void* y, cora_dtype_t dt,
+                                  cudaStream_t stream) {
+  const int64_t n_rows = static_cast<int64_t>(L.total_tokens) * L.heads;
+  if (n_rows == 0) return cudaSuccess;
+  const dim3 block(256), grid(static_cast<unsigned>((n_rows + 7) / 8));
+  if (dt == CORA_DT_BF16)
+    ragged_softmax_kernel<__nv_bfloat16, 16><<<grid, block, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), L.lengths, L.attn_off, L.seq_of_tok,
+        L.pos_in_seq, L.heads, n_rows);
+  else
+    ragged_softmax_kernel<float, 16><<<grid, block, 0, stream>>>(static_cast<const float*>(x),
+                                                                 static_cast<float*>(y), L.lengths, L.attn_off,
+                                                                 L.seq_of_tok, L.pos_in_seq, L.heads, n_rows);
+  return cudaGetLastError();
+}
+
+}  // namespace cora

@@ -1,0 +1,188 @@
+// Step a1: the "prelude" of CoRa as device kernels.
+//
+// CoRa builds its auxiliary arrays (A_d prefix sums, App. B.1, and the
+// vloop-fusion maps f_fo / f_fi / f_oif, App. B.2) on the HOST and copies
+// them to the GPU; that copy is "the major source of the overhead".
+// Here the tables are computed on the device from the lengths, so only B lengths (or nothing,
+// if they already live on the GPU) cross PCIe.
+//
+//   kernel 1 (one CTA, 1024 threads): block scans of L and L^2 -> row_off, attn_off;
+//            validation -> status; longest-first attention tile list (PAPER.md:1747-1750,
+//            reading c15: key (-ceil(L/128), b, h, qt)) by a stable counting sort.
+//   kernel 2 (grid over T): f_fo / f_fi by binary search of row_off.
+#include <cstdint>
+
+#include "cora_internal.h"
+
+namespace cora {
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kMaxBuckets = 129;  // ceil(16383/128) + 1 distinct q-tile counts
+
+template <typename T>
+__device__ T block_exclusive_scan(T v, T* warp_sums, T& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T s = warp_sums[lane];  // 32 warps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sums[lane] = s;  // inclusive over warps
+  }
+  __syncthreads();
+  T warp_prefix = wid ? warp_sums[wid - 1] : T(0);
+  total = warp_sums[31];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t* __restrict__ lengths, int32_t batch,
+                                                                   int32_t total_tokens, int32_t heads,
+                                                                   int32_t max_len, int32_t* __restrict__ row_off,
+                                                                   int64_t* __restrict__ attn_off,
+                                                                   int32_t* __restrict__ tiles,
+                                                                   int32_t* __restrict__ n_tiles,
+                                                                   int32_t* __restrict__ status) {
+  __shared__ int64_t ws64[32];
+  __shared__ int32_t ws32[32];
+  __shared__ int32_t hist[kMaxBuckets];
+  __shared__ int32_t bucket_base[kMaxBuckets];
+  __shared__ int32_t running[kMaxBuckets];
+  __shared__ int32_t warp_cnt[32][kMaxBuckets];
+  __shared__ int32_t s_bad;
+  __shared__ unsigned long long s_raw_sum;  // sum of the raw (unclamped) lengths, for the T check
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < kMaxBuckets; i += kScanThreads) {
+    hist[i] = 0;
+    running[i] = 0;
+  }
+  if (tid == 0) {
+    s_bad = 0;
+    s_raw_sum = 0ull;
+  }
+  __syncthreads();
+
+  // ---- pass 1: prefix sums (A_1 arrays) + validation + bucket histogram
+  int32_t carry32 = 0;
+  int64_t carry64 = 0;
+  for (int base = 0; base < batch; base += kScanThreads) {
+    const int b = base + tid;
+    int32_t L = 0;
+    if (b < batch) {
+      L = lengths[b];
+      atomicAdd(&s_raw_sum, static_cast<unsigned long long>(static_cast<int64_t>(L)));
+      if (L < 0 || L > max_len) {
+        s_bad = 1;  // benign race: every writer stores 1
+        L = L < 0 ? 0 : max_len;
+      }
+    }
+    int32_t tot32;
+    int64_t tot64;
+    const int32_t ex32 = block_exclusive_scan<int32_t>(L, ws32, tot32);
+    const int64_t ex64 = block_exclusive_scan<int64_t>(static_cast<int64_t>(L) * L, ws64, tot64);
+    if (b < batch) {
+      row_off[b] = carry32 + ex32;
+      attn_off[b] = carry64 + ex64;
+      atomicAdd(&hist[(L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS], 1);
+    }
+    carry32 += tot32;
+    carry64 += tot64;
+  }
+  __syncthreads();
+  int32_t st = 0;
+  if (s_bad) st |= CORA_STATUS_BAD_LENGTH;
+  if (static_cast<int64_t>(s_raw_sum) != total_tokens) st |= CORA_STATUS_SUM_MISMATCH;
+  if (tid == 0) {
+    row_off[batch] = carry32;
+    attn_off[batch] = carry64;
+    *status = st;
+    // bucket bases in descending tile-count order
+    int32_t acc = 0;
+    for (int v = kMaxBuckets - 1; v >= 0; --v) {
+      bucket_base[v] = acc;
+      acc += heads * v * hist[v];
+    }
+    *n_tiles = st ? 0 : acc;
+  }
+  if (st) return;  // data error: empty work list, nothing else is read
+  __syncthreads();
+
+  // ---- pass 2: stable rank of each sequence inside its bucket -> tile list
+  for (int base = 0; base < batch; base += kScanThreads) {
+    const int b = base + tid;
+    const bool valid = b < batch;
+    const int32_t L = valid ? lengths[b] : 0;
+    const int32_t v = valid ? (L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS : -1;
+    for (int i = tid; i < 32 * kMaxBuckets; i += kScanThreads) (&warp_cnt[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t same = __match_any_sync(0xffffffffu, v);
+    const int rank_in_warp = __popc(same & ((1u << lane) - 1u));
+    if (valid && rank_in_warp == 0) warp_cnt[wid][v] = __popc(same);
+    __syncthreads();
+    if (valid && v > 0) {
+      int32_t rank = running[v] + rank_in_warp;
+      for (int w = 0; w < wid; ++w) rank += warp_cnt[w][v];
+      int32_t* out = tiles + bucket_base[v] + rank * heads * v;
+      for (int h = 0; h < heads; ++h)
+        for (int qt = 0; qt < v; ++qt) out[h * v + qt] = b | (h << 16) | (qt << 24);
+    }
+    __syncthreads();
+    for (int u = tid; u < kMaxBuckets; u += kScanThreads) {
+      int32_t s = 0;
+      for (int w = 0; w < 32; ++w) s += warp_cnt[w][u];
+      running[u] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// f_fo / f_fi: for token t, b = max{b : row_off[b] <= t} (skips empty sequences), i = t - row_off[b].
+__global__ void fusion_maps_kernel(const int32_t* __restrict__ row_off, const int32_t* __restrict__ status,
+                                   int32_t batch, int32_t total_tokens, int32_t* __restrict__ seq_of_tok,
+                                   int32_t* __restrict__ pos_in_seq) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total_tokens) return;
+  if (*status != 0) {
+    seq_of_tok[t] = -1;
+    pos_in_seq[t] = -1;
+    return;
+  }
+  int lo = 0, hi = batch;  // invariant: row_off[lo] <= t < row_off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (row_off[mid] <= t)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  seq_of_tok[t] = lo;
+  pos_in_seq[t] = t - row_off[lo];
+}
+
+}  // namespace
+
+void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
+                         const cora_layout_t& L, cudaStream_t stream) {
+  layout_scan_kernel<<<1, kScanThreads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off,
+                                                     L.attn_off, L.tiles, L.n_tiles, L.status);
+  if (total_tokens > 0) {
+    const int threads = 256;
+    fusion_maps_kernel<<<(total_tokens + threads - 1) / threads, threads, 0, stream>>>(
+        L.row_off, L.status, batch, total_tokens, L.seq_of_tok, L.pos_in_seq);
+  }
+}
+
+}  // namespace cora

@@ -1,0 +1,259 @@
+"""GPU parity: every step of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star, reading c12): offset tables and indexing
+bit-exact; bf16 tensor-core outputs max relative error <= 2e-2; fp32 elementwise <= 1e-5.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from util import TOL_BF16, TOL_F32, bf16_cuda, f32_cuda, rel_err, to_np
+
+pytestmark = pytest.mark.gpu
+
+EDGE_LENGTHS = [1, 63, 64, 65, 127, 128, 129, 511, 512]
+
+
+def P():
+    import paper_2110_10221_b200 as P
+    return P
+
+
+def _layout(lengths, heads, max_len=512):
+    Lt = torch.tensor(np.asarray(lengths, np.int32), device="cuda")
+    return P().layout_build(Lt, int(np.sum(lengths)), heads, max_len)
+
+
+# ---------------------------------------------------------------- a1: prelude (bit-exact)
+LAYOUT_CASES = [
+    [3, 7, 1, 5],
+    [0, 4, 0, 1, 2],
+    EDGE_LENGTHS,
+    [512] * 64,
+    list(synth.config("C4-wiki512")[0]),
+    list(synth.config("C2-mnli")[0]),
+    list(synth.uniform_lengths(3000, 0, 700, seed=5)),  # > 1024 sequences: multi-chunk scan
+    [0],
+    [],
+]
+
+
+@pytest.mark.parametrize("lengths", LAYOUT_CASES, ids=lambda l: f"B{len(l)}")
+@pytest.mark.parametrize("heads", [1, 8])
+def test_layout_tables_bit_exact(lengths, heads):
+    lay = _layout(lengths, heads, max_len=1024)
+    tb = {k: v.cpu().numpy() for k, v in lay.tables().items()}
+    assert lay.status() == 0
+    assert tb["row_off"].tolist() == oracle.row_offsets(lengths)
+    assert tb["attn_off"].tolist() == oracle.attn_offsets(lengths)
+    f_fo, f_fi, _ = oracle.fusion_maps(lengths)
+    assert tb["seq_of_tok"].tolist() == f_fo
+    assert tb["pos_in_seq"].tolist() == f_fi
+    n = int(tb["n_tiles"][0])
+    ref = oracle.tile_list(lengths, heads)
+    assert n == len(ref) <= lay.c.n_tiles_max
+    w = tb["tiles"][:n].astype(np.int64)
+    got = list(zip((w & 0xFFFF).tolist(), ((w >> 16) & 0xFF).tolist(), ((w >> 24) & 0x7F).tolist()))
+    assert got == ref
+
+
+@pytest.mark.parametrize("lengths,T,max_len,expect", [
+    ([3, 7, 1, 5], 17, 512, oracle.STATUS_SUM_MISMATCH),
+    ([3, -1, 1, 5], 8, 512, oracle.STATUS_BAD_LENGTH),
+    ([3, 600], 603, 512, oracle.STATUS_BAD_LENGTH),
+    ([3, 600], 5, 512, oracle.STATUS_BAD_LENGTH | oracle.STATUS_SUM_MISMATCH),
+])
+def test_layout_status_word(lengths, T, max_len, expect):
+    Lt = torch.tensor(np.asarray(lengths, np.int32), device="cuda")
+    lay = P().layout_build(Lt, T, 2, max_len)
+    assert lay.status() == 2  # CORA_ERR_DATA
+    tb = lay.tables()
+    assert int(tb["status"][0]) == expect == oracle.validate_lengths(lengths, T, max_len)
+    assert int(tb["n_tiles"][0]) == 0  # empty work list: nothing downstream runs
+
+
+# ---------------------------------------------------------------- a5/a8: LayerNorm
+@pytest.mark.parametrize("rows,cols", [(1, 512), (333, 512), (17, 16), (5, 2048), (9, 4096)])
+@pytest.mark.parametrize("use_res", [False, True])
+def test_layernorm_fp32(rows, cols, use_res):
+    x = synth.normal((rows, cols), 1).astype(np.float32).astype(np.float64) * 2 + 0.5
+    r = synth.normal((rows, cols), 2).astype(np.float32).astype(np.float64) if use_res else None
+    g = synth.normal((cols,), 3).astype(np.float32).astype(np.float64)
+    b = synth.normal((cols,), 4).astype(np.float32).astype(np.float64)
+    y = P().layernorm(f32_cuda(x), f32_cuda(g), f32_cuda(b), residual=f32_cuda(r) if use_res else None)
+    ref = oracle.layernorm(x + (r if use_res else 0), g, b, 1e-5)
+    assert rel_err(to_np(y), ref) <= TOL_F32
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 512), (17, 16)])
+def test_layernorm_bf16(rows, cols):
+    x = synth.round_bf16(synth.normal((rows, cols), 5))
+    g, b = synth.round_f32(1 + 0.1 * synth.normal((cols,), 6)), synth.round_f32(0.1 * synth.normal((cols,), 7))
+    y = P().layernorm(bf16_cuda(x), f32_cuda(g), f32_cuda(b))
+    assert rel_err(to_np(y), oracle.layernorm(x, g, b)) <= TOL_BF16
+
+
+# ---------------------------------------------------------------- a3': standalone ragged softmax
+@pytest.mark.parametrize("lengths", [[3, 7, 1, 5], [0, 40, 0, 3], EDGE_LENGTHS, [600, 1, 1000]])
+def test_ragged_softmax_fp32(lengths):
+    H, d = 2, 16
+    qkv = synth.normal((sum(lengths), 3 * d), 11)
+    x = oracle.attention_scores_ragged(qkv, lengths, H).astype(np.float32).astype(np.float64)
+    lay = _layout(lengths, H, max_len=1024)
+    y = P().ragged_softmax(lay, f32_cuda(x))
+    assert rel_err(to_np(y), oracle.ragged_softmax(x, lengths, H)) <= TOL_F32
+
+
+def test_ragged_softmax_bf16_c2():
+    lengths = list(synth.config("C2-mrpc")[0])
+    H, d = 8, 512
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 12))
+    x = synth.round_bf16(oracle.attention_scores_ragged(qkv, lengths, H))
+    lay = _layout(lengths, H)
+    y = P().ragged_softmax(lay, bf16_cuda(x))
+    assert rel_err(to_np(y), oracle.ragged_softmax(x, lengths, H)) <= TOL_BF16
+
+
+# ---------------------------------------------------------------- a2/a4/a6/a7: tcgen05 GEMM
+GEMM_SHAPES = [
+    (128, 256, 64), (300, 1536, 512), (1000, 512, 2048), (257, 2048, 512), (16, 48, 16), (16, 16, 32),
+    (1, 512, 512), (4099, 512, 512), (200, 264, 72),
+]
+
+
+@pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
+def test_linear_plain(m, n, k):
+    a = synth.round_bf16(synth.normal((m, k), 21))
+    w = synth.round_bf16(synth.normal((n, k), 22) / math.sqrt(k))
+    c = P().linear(bf16_cuda(a), bf16_cuda(w))
+    assert rel_err(to_np(c), oracle.linear(a, w)) <= TOL_BF16
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+@pytest.mark.parametrize("use_res", [False, True])
+def test_linear_epilogues(act, use_res):
+    m, n, k = 333, 512, 512
+    a = synth.round_bf16(synth.normal((m, k), 23))
+    w = synth.round_bf16(synth.normal((n, k), 24) / math.sqrt(k))
+    b = synth.round_bf16(synth.normal((n,), 25))
+    r = synth.round_bf16(synth.normal((m, n), 26)) if use_res else None
+    c = P().linear(bf16_cuda(a), bf16_cuda(w), bias=bf16_cuda(b), residual=bf16_cuda(r) if use_res else None, act=act)
+    ref = oracle.linear(a, w, b, residual=r, act=None if act == "none" else act)
+    assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
+# ---------------------------------------------------------------- a3: fused ragged attention
+ATTN_CASES = [
+    [3, 7, 1, 5],
+    EDGE_LENGTHS,
+    [0, 130, 0, 1, 0],
+    [512],
+    [200] * 7,
+    list(synth.config("C2-mnli")[0]),
+    list(synth.config("C2-mrpc")[0]),
+]
+
+
+@pytest.mark.parametrize("lengths", ATTN_CASES, ids=lambda l: f"B{len(l)}-T{sum(l)}")
+@pytest.mark.parametrize("head_dim,heads", [(64, 8), (64, 2), (8, 2), (32, 4)])
+def test_ragged_attention(lengths, head_dim, heads):
+    d = heads * head_dim
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 31))
+    lay = _layout(lengths, heads)
+    o = P().ragged_attention(lay, bf16_cuda(qkv), head_dim)
+    assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, heads)) <= TOL_BF16
+
+
+def test_attention_poisoned_output_untouched_rows_none():
+    # every output row belongs to some sequence: all are written; NaN-poison must disappear
+    lengths = [5, 0, 129, 64]
+    H, hd = 8, 64
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * H * hd), 32))
+    lay = _layout(lengths, H)
+    out = torch.full((sum(lengths), H * hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    P().ragged_attention(lay, bf16_cuda(qkv), hd, out=out)
+    assert torch.isfinite(out).all()
+
+
+# ---------------------------------------------------------------- whole layer
+def _layer_case(name, act="relu", subsample=None):
+    lengths, d, H, dff = synth.config(name)
+    w = synth.encoder_weights(d, H, dff)
+    x = synth.activations(int(lengths.sum()), d)
+    params = P().EncoderParams.from_host(w, act=act)
+    lay = _layout(lengths, H)
+    y = P().encoder_layer(bf16_cuda(x), lay, params)
+    return lengths, w, x, to_np(y)
+
+
+@pytest.mark.parametrize("act", ["relu", "gelu"])
+def test_layer_c1(act):
+    lengths, w, x, y = _layer_case("C1", act)
+    assert rel_err(y, oracle.encoder_layer(x, lengths, w, act=act)) <= TOL_BF16
+
+
+def test_layer_c3():
+    lengths, w, x, y = _layer_case("C3")
+    assert rel_err(y, oracle.encoder_layer(x, lengths, w)) <= TOL_BF16
+
+
+def test_layer_c4_sampled_sequences():
+    lengths, w, x, y = _layer_case("C4-wiki512")
+    ro = oracle.row_offsets(lengths)
+    # oracle one sequence at a time on a sample (the longest, shortest and a few others)
+    order = np.argsort(lengths)
+    sample = sorted(set([int(order[0]), int(order[-1]), 0, 37, 64, 127]))
+    for b in sample:
+        L = int(lengths[b])
+        ref = oracle.encoder_layer(x[ro[b]:ro[b] + L], [L], w)
+        assert rel_err(y[ro[b]:ro[b] + L], ref) <= TOL_BF16, b
+
+
+# ---------------------------------------------------------------- GPU self-consistency (bitwise)
+def test_layer_sequence_independence_and_permutation():
+    lengths = np.array([100, 7, 300, 1, 129, 64])
+    d, H, dff = 512, 8, 2048
+    w = synth.encoder_weights(d, H, dff)
+    x = synth.activations(int(lengths.sum()), d)
+    params = P().EncoderParams.from_host(w)
+    layer = P().EncoderLayer(params)
+    ro = oracle.row_offsets(lengths)
+    y = layer(bf16_cuda(x), _layout(lengths, H)).cpu()
+    # deterministic
+    y2 = layer(bf16_cuda(x), _layout(lengths, H)).cpu()
+    assert torch.equal(y, y2)
+    # perturb sequence 2: every other sequence's rows are bitwise unchanged
+    x2 = x.copy()
+    x2[ro[2]:ro[3]] = synth.round_bf16(x2[ro[2]:ro[3]] + 1.0)
+    y3 = layer(bf16_cuda(x2), _layout(lengths, H)).cpu()
+    keep = np.ones(len(y), bool)
+    keep[ro[2]:ro[3]] = False
+    assert torch.equal(y[keep], y3[keep])
+    # batch permutation: reordering sequences reorders the outputs bitwise
+    perm = [3, 0, 5, 2, 4, 1]
+    xp = np.concatenate([x[ro[b]:ro[b + 1]] for b in perm])
+    yp = layer(bf16_cuda(xp), _layout(lengths[perm], H)).cpu()
+    ref = torch.cat([y[ro[b]:ro[b + 1]] for b in perm])
+    assert torch.equal(yp, ref)
+
+
+def test_layer_virtual_ranks_equal_single_gpu():
+    # the G-shard path (each rank runs its contiguous sequence range) reproduces the 1-GPU output bitwise
+    lengths, d, H, dff = synth.config("C3")
+    w = synth.encoder_weights(d, H, dff)
+    x = synth.activations(int(lengths.sum()), d)
+    layer = P().EncoderLayer(P().EncoderParams.from_host(w))
+    ro = oracle.row_offsets(lengths)
+    y = layer(bf16_cuda(x), _layout(lengths, H)).cpu()
+    for G in (2, 4, 8):
+        plan = P().shard_plan(list(lengths), d, dff, G)
+        parts = []
+        for r in range(G):
+            b0, b1 = plan[r], plan[r + 1]
+            if b1 > b0:
+                parts.append(layer(bf16_cuda(x[ro[b0]:ro[b1]]), _layout(lengths[b0:b1], H)).cpu())
+        assert torch.equal(torch.cat(parts), y)
