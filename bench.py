@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the ragged encoder layer (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4-wiki512] [--impl cora|reference]
+
+A "step" is one pass of the whole hot path over one synthetic ragged batch: the device prelude
+(a1: offset tables + tile list) followed by the seven layer kernels (a2..a8), and for N > 1 the
+final NCCL all-gather of the ragged outputs.  The batch is the configuration BASELINE.json's
+metric is quoted on: bs 128, Wiki512-like lengths (configs[3], "C4").  Metric: useful (unpadded)
+TFLOP/s = (2 T (4 d^2 + 2 d d_ff) + 4 d sum L^2) / step time; ms/step is reported beside it.
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the launching
+stream, with a 256 MB L2 flush between steps (outside the events); barrier + synchronize on both
+sides; the max over ranks.  `--impl reference` times the fp64 CPU oracle instead (the reference
+arm of this tier: a deliberately slow program).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "ragged encoder layer useful TFLOP/s (bf16, unpadded FLOPs)"
+KERNELS = ["qkv_gemm", "attention", "out_proj_gemm", "layernorm1", "ff1_gemm", "ff2_gemm", "layernorm2"]
+
+
+def useful_flops(lengths, d, dff) -> int:
+    T = int(np.sum(lengths))
+    S2 = int(np.sum(np.asarray(lengths, np.int64) ** 2))
+    return 2 * T * (4 * d * d + 2 * d * dff) + 4 * d * S2
+
+
+def padded_flops(lengths, d, dff) -> int:
+    Lp = int(np.max(lengths))
+    return useful_flops([Lp] * len(lengths), d, dff)
+
+
+def kernel_work(name, T, S2, d, dff):
+    """(bound, algorithmic amount per launch, unit) for each layer kernel."""
+    if name == "qkv_gemm":
+        return "tensor", 2.0 * T * d * 3 * d, "flop"
+    if name == "attention":
+        return "tensor", 4.0 * d * S2, "flop"
+    if name == "out_proj_gemm":
+        return "tensor", 2.0 * T * d * d, "flop"
+    if name == "ff1_gemm":
+        return "tensor", 2.0 * T * d * dff, "flop"
+    if name == "ff2_gemm":
+        return "tensor", 2.0 * T * dff * d, "flop"
+    # LayerNorm: read + write one bf16 row each, gamma/beta once
+    return "hbm", 2.0 * T * d * 2 + 2 * d * 4, "byte"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"bf16_tflops": j["bf16_tflops"], "bf16_tflops_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                "hbm_gbs": j["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    # B200_PROFILING.md fallback
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled"], "samples": 0}
+        time.sleep(0.05)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+                if any(r[2].replace(".", "").isdigit() for r in rows) else None}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def oracle_sample(lengths, w, x, budget_s: float):
+    """Time the fp64 oracle on a bounded sample of the workload's sequences (seeded order)."""
+    import oracle
+
+    ro = oracle.row_offsets(lengths)
+    order = np.random.default_rng(0).permutation(len(lengths))
+    done, flops, t_total, n = [], 0, 0.0, 0
+    for b in order:
+        L = int(lengths[b])
+        if L == 0:
+            continue
+        t0 = time.perf_counter()
+        oracle.encoder_layer(x[ro[b]:ro[b] + L], [L], w)
+        t_total += time.perf_counter() - t0
+        flops += useful_flops([L], w.d_model, w.d_ff)
+        n += 1
+        done.append(L)
+        if t_total >= budget_s:
+            break
+    return flops, t_total, n, done
+
+
+def run_reference(args, lengths, d, H, dff, world, rank):
+    """The reference arm of this tier: the fp64 CPU oracle on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    w = synth.encoder_weights(d, H, dff)
+    x = synth.activations(int(lengths.sum()), d)
+    per_step_budget = max(0.5, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(lengths, w, x, per_step_budget / 4)
+    times, flops_all, nseq = [], [], 0
+    for _ in range(args.steps):
+        f, t, n, _ = oracle_sample(lengths, w, x, per_step_budget)
+        times.append(t)
+        flops_all.append(f)
+        nseq = n
+    value = sum(flops_all) / sum(times) / 1e12
+    ms = 1e3 * sum(times) / len(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "batch": int(len(lengths)), "total_tokens": int(lengths.sum()),
+                   "d_model": d, "heads": H, "d_ff": dff, "parallelism": "host"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"{nseq} of {len(lengths)} sequences per step (seeded permutation), fp64 NumPy"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C4-wiki512")
+    ap.add_argument("--impl", default="cora", choices=["cora", "reference"])
+    ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "cora" and os.environ.get("CORA_ALLOW_FEW_WARMUP") is None:
+        args.warmup = 3
+
+    world, rank, local = dist_setup()
+    lengths, d, H, dff = synth.config(args.config)
+    lengths = np.asarray(lengths, np.int64)
+
+    if args.impl == "reference":
+        run_reference(args, lengths, d, H, dff, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_10221_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---------------------------------------------------------------- workload (synthetic, seeded)
+    w = synth.encoder_weights(d, H, dff)
+    x_all = synth.activations(int(lengths.sum()), d)
+    ro = np.concatenate([[0], np.cumsum(lengths)])
+    plan = P.shard_plan(list(lengths), d, dff, world)
+    b0, b1 = plan[rank], plan[rank + 1]
+    loc_len = lengths[b0:b1]
+    T_loc = int(loc_len.sum())
+    tok_begin = [int(ro[plan[r]]) for r in range(world + 1)]
+    x_loc = x_all[ro[b0]:ro[b1]]
+    params = P.EncoderParams.from_host(w, device=dev)
+    layer = P.EncoderLayer(params)
+    len_dev = torch.tensor(loc_len, dtype=torch.int32, device=dev)
+    x_dev = torch.tensor(x_loc, dtype=torch.float32).to(torch.bfloat16).to(dev) if T_loc else \
+        torch.empty(0, d, dtype=torch.bfloat16, device=dev)
+    y_dev = torch.empty(T_loc, d, dtype=torch.bfloat16, device=dev)
+    y_full = torch.empty(int(lengths.sum()), d, dtype=torch.bfloat16, device=dev) if world > 1 else y_dev
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(events=None):
+        lay = P.layout_build(len_dev, T_loc, H, 512) if len(loc_len) else None
+        if lay is not None and T_loc:
+            layer(x_dev, lay, out=y_dev, events=events)
+        elif events is not None:
+            for e in events:
+                e.record()
+        if world > 1:
+            if T_loc:
+                y_full[tok_begin[rank]:tok_begin[rank + 1]].copy_(y_dev)
+            for r in range(world):
+                if tok_begin[r + 1] > tok_begin[r]:
+                    dist.broadcast(y_full[tok_begin[r]:tok_begin[r + 1]], src=r)
+        return lay
+
+    # correctness gate on the benchmarked configuration (status word)
+    lay = step()
+    if lay is not None:
+        assert lay.status() == 0, "layout status != 0"
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    n_ev = P._lib.LAYER_EVENTS
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if not args.no_clocks:
+        sampler.start()
+        time.sleep(0.1)
+    try:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            if not args.no_flush:
+                flush.zero_()
+            step_ev[i][0].record(stream)
+            step(kern_ev[i])
+            step_ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    finally:
+        clocks = sampler.stop()
+
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    ms_local = float(np.mean(step_ms))
+    kern_ms = {k: float(np.mean([ev[j].elapsed_time(ev[j + 1]) for ev in kern_ev])) for j, k in enumerate(KERNELS)}
+    prelude_ms = float(np.mean([a.elapsed_time(ev[0]) for (a, _), ev in zip(step_ev, kern_ev)]))
+    if world > 1:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    else:
+        ms = ms_local
+
+    # ---------------------------------------------------------------- e2e: host buffers through the C ABI
+    e2e = None
+    if not args.no_e2e and T_loc:
+        hf = P.HostForward(params, len(loc_len), T_loc, 512, device=dev)
+        len_h = torch.tensor(loc_len, dtype=torch.int32).pin_memory()
+        x_h = torch.tensor(x_loc, dtype=torch.float32).to(torch.bfloat16).pin_memory()
+        y_h = torch.empty(T_loc, d, dtype=torch.bfloat16).pin_memory()
+        for _ in range(args.warmup):
+            hf(len_h, x_h, y_h)
+        torch.cuda.synchronize()
+        assert hf.status() == 0
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            if not args.no_flush:
+                flush.zero_()
+            ev[i][0].record(stream)
+            hf(len_h, x_h, y_h)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": useful_flops(lengths, d, dff) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(x_h.numel() * 2 + len_h.numel() * 4),
+               "d2h_bytes_per_step": int(y_h.numel() * 2), "path": "cora_encoder_forward_host (pinned host buffers)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    total_flops = useful_flops(lengths, d, dff)
+    value = total_flops / (ms * 1e-3) / 1e12
+    T, S2 = int(loc_len.sum()), int((loc_len ** 2).sum())
+    kernels = {}
+    for k in KERNELS:
+        bound, work, unit = kernel_work(k, T, S2, d, dff)
+        dur = kern_ms[k] * 1e-3
+        if bound == "tensor":
+            ach = work / dur / 1e12
+            peak = peaks["bf16_tflops_sustained"]
+            kernels[k] = {"ms": kern_ms[k], "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                          "frac": ach / peak}
+        else:
+            ach = work / dur / 1e9
+            peak = peaks["hbm_gbs"]
+            kernels[k] = {"ms": kern_ms[k], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                          "frac": ach / peak}
+    dom = max(KERNELS, key=lambda k: kern_ms[k])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    roofline = {"kernel": dom, "bound": kernels[dom]["bound"], "achieved": kernels[dom]["achieved"],
+                "peak": kernels[dom]["peak"], "unit": kernels[dom]["unit"], "frac": kernels[dom]["frac"],
+                "traffic": traffic, "peak_source": peaks["source"] + (" sustained" if kernels[dom]["bound"] == "tensor" else "")}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        lengths_c, _, _, _ = synth.config(args.config)
+        f, t, n, _ = oracle_sample(np.asarray(lengths_c), w, x_all, args.cpu_budget)
+        cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"{n} of {len(lengths)} sequences of {args.config} (seeded permutation), fp64 NumPy, "
+                         f"{t:.1f} s"}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": args.config, "batch": int(len(lengths)), "total_tokens": int(lengths.sum()),
+                   "sum_L2": int((lengths ** 2).sum()), "max_len": int(lengths.max()), "d_model": d, "heads": H,
+                   "d_ff": dff, "parallelism": f"seq-shard{world}" if world > 1 else "single",
+                   "l2": "no flush" if args.no_flush else "flushed (256 MB write) between steps",
+                   "step": "prelude(a1) + 7 layer kernels (a2..a8)" + (" + NCCL all-gather" if world > 1 else "")},
+        "frac_of_peak": {"burst": value / peaks["bf16_tflops"], "sustained": value / peaks["bf16_tflops_sustained"],
+                         "source": peaks["source"]},
+        "padded_over_useful_flops": padded_flops(lengths, d, dff) / total_flops,
+        "roofline": roofline,
+        "kernels": kernels,
+        "prelude_ms": prelude_ms,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 9 * args.steps,
+        "clocks": clocks,
+        "paper_context": {"cora_v100_fp32_ms_wiki512_bs128": 32.17, "ft_eff_v100_fp32_ms": 33.66,
+                          "source": "PAPER.md:870-872 (Table 4), other hardware and precision"},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -148,6 +148,30 @@ size_t cora_encoder_workspace_bytes(const cora_encoder_params_t* p, int32_t tota
 cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
                                      void* y, void* ws, size_t ws_bytes, void* stream);
 
+/* Number of events cora_encoder_layer_fwd_ex records (one before each of the 7 kernels + one after). */
+#define CORA_LAYER_EVENTS 8
+
+/* Same as cora_encoder_layer_fwd; when `events` is non-NULL it points to CORA_LAYER_EVENTS
+ * cudaEvent_t handles (caller-created) and event k is recorded on `stream` right before kernel k
+ * (0 QKV GEMM, 1 attention, 2 out-proj GEMM, 3 LN1, 4 FF1 GEMM, 5 FF2 GEMM, 6 LN2) and event 7
+ * after the last one, so the caller can time every kernel of the layer on the launching stream. */
+cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
+                                        void* y, void* ws, size_t ws_bytes, void* stream, void* const* events);
+
+/* Workspace for cora_encoder_forward_host (device lengths + X + Y + layout tables + layer workspace). */
+size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
+                                         int32_t max_len);
+
+/* End-to-end call with HOST buffers: copies lengths_host[batch] (int32) and x_host[T, d] (bf16)
+ * host->device, builds the layout (step a1), runs the layer (a2..a8) and copies y_host[T, d] back,
+ * all enqueued on `stream` (asynchronous when the host buffers are pinned; the caller synchronises
+ * the stream before reading y_host).  The device status word is not read (no hidden sync): call
+ * cora_layout_status on *layout_out after synchronising to detect data errors.  layout_out may be
+ * NULL.  T = total_tokens must equal sum(lengths_host) (checked on the device). */
+cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
+                                        int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host,
+                                        void* ws, size_t ws_bytes, cora_layout_t* layout_out, void* stream);
+
 /* ---------------------------------------------------------------- op-level entry points */
 
 /* c[m, n] = act(a[m, k] w[n, k]^T + bias[n]) + residual[m, n]  (bf16, fp32 accumulate in TMEM).

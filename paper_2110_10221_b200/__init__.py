@@ -8,6 +8,7 @@ from . import _lib
 from .api import (  # noqa: F401
     EncoderLayer,
     EncoderParams,
+    HostForward,
     RaggedLayout,
     build_info,
     encoder_layer,

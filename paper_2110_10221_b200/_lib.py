@@ -1,7 +1,7 @@
 """ctypes view of libcora_b200.so (include/cora.h).  Argument marshalling only.
 
 There is no fallback: if the shared library is missing or fails to load, importing the
-binding raises.  Build it with `python -m paper_2110_10221_b200.build` (or
+binding raises.  Build it with `python paper_2110_10221_b200/build.py` (or
 `__graft_entry__.build()`).
 """
 from __future__ import annotations
@@ -17,11 +17,13 @@ CORA_DT_BF16, CORA_DT_F32 = 0, 1
 CORA_ACT_NONE, CORA_ACT_RELU, CORA_ACT_GELU_ERF = 0, 1, 2
 CORA_STATUS_BAD_LENGTH, CORA_STATUS_SUM_MISMATCH = 1, 2
 TILE_ROWS = 128
+LAYER_EVENTS = 8
 
 # Every symbol include/cora.h declares (checked by tests/test_boundary.py on CPU).
 EXPORTS = (
     "cora_layout_workspace_bytes", "cora_layout_build", "cora_layout_status", "cora_encoder_workspace_bytes",
-    "cora_encoder_layer_fwd", "cora_linear_fwd", "cora_ragged_attention_fwd", "cora_ragged_softmax_fwd",
+    "cora_encoder_layer_fwd", "cora_encoder_layer_fwd_ex", "cora_forward_host_workspace_bytes",
+    "cora_encoder_forward_host", "cora_linear_fwd", "cora_ragged_attention_fwd", "cora_ragged_softmax_fwd",
     "cora_layernorm_fwd", "cora_shard_plan", "cora_status_string", "cora_device_sm_count", "cora_build_info",
 )
 
@@ -64,7 +66,7 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2110_10221_b200.build`")
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python paper_2110_10221_b200/build.py`")
         L = ctypes.CDLL(LIB_PATH)
         vp, i32, sz, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t, ctypes.c_float
         sig = {
@@ -73,6 +75,11 @@ def lib() -> ctypes.CDLL:
             "cora_layout_status": (i32, [ctypes.POINTER(Layout), vp]),
             "cora_encoder_workspace_bytes": (sz, [ctypes.POINTER(EncoderParams), i32]),
             "cora_encoder_layer_fwd": (i32, [ctypes.POINTER(EncoderParams), ctypes.POINTER(Layout), vp, vp, vp, sz, vp]),
+            "cora_encoder_layer_fwd_ex": (i32, [ctypes.POINTER(EncoderParams), ctypes.POINTER(Layout), vp, vp, vp, sz, vp,
+                                                ctypes.POINTER(ctypes.c_void_p)]),
+            "cora_forward_host_workspace_bytes": (sz, [ctypes.POINTER(EncoderParams), i32, i32, i32]),
+            "cora_encoder_forward_host": (i32, [ctypes.POINTER(EncoderParams), vp, i32, i32, i32, vp, vp, vp, sz,
+                                                ctypes.POINTER(Layout), vp]),
             "cora_linear_fwd": (i32, [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]),
             "cora_ragged_attention_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, f32, vp]),
             "cora_ragged_softmax_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, vp]),

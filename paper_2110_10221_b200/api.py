@@ -143,7 +143,8 @@ class EncoderLayer:
         return C.lib().cora_encoder_workspace_bytes(ctypes.byref(self.cp), int(total_tokens))
 
     def __call__(self, x: torch.Tensor, layout: RaggedLayout, out: Optional[torch.Tensor] = None,
-                 stream=None) -> torch.Tensor:
+                 stream=None, events: Optional[Sequence["torch.cuda.Event"]] = None) -> torch.Tensor:
+        """events: optional C.LAYER_EVENTS torch.cuda.Event objects recorded around every kernel."""
         _need_cuda(x)
         T = layout.total_tokens
         if x.dtype != torch.bfloat16 or x.shape != (T, self.params.d_model):
@@ -152,10 +153,45 @@ class EncoderLayer:
         if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
             self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)
         y = torch.empty_like(x) if out is None else out
-        C.check(C.lib().cora_encoder_layer_fwd(ctypes.byref(self.cp), ctypes.byref(layout.c), _ptr(x), _ptr(y),
-                                               _ptr(self.ws), self.ws.numel(), _stream(stream)),
-                "cora_encoder_layer_fwd")
+        ev = None
+        if events is not None:
+            if len(events) != C.LAYER_EVENTS:
+                raise ValueError(f"need {C.LAYER_EVENTS} events")
+            for e in events:  # torch creates its CUDA events lazily, on first record
+                if e.cuda_event == 0:
+                    e.record(stream)
+            ev = (ctypes.c_void_p * C.LAYER_EVENTS)(*[e.cuda_event for e in events])
+        C.check(C.lib().cora_encoder_layer_fwd_ex(ctypes.byref(self.cp), ctypes.byref(layout.c), _ptr(x), _ptr(y),
+                                                  _ptr(self.ws), self.ws.numel(), _stream(stream), ev),
+                "cora_encoder_layer_fwd_ex")
         return y
+
+
+class HostForward:
+    """End-to-end public call with HOST buffers (cora_encoder_forward_host): H2D of lengths and x,
+    device prelude, the layer, D2H of y -- one C call, enqueued on the stream."""
+
+    def __init__(self, params: EncoderParams, batch: int, total_tokens: int, max_len: int = 512, device="cuda"):
+        self.params = params
+        self.cp = params.cstruct()
+        self.batch, self.total_tokens, self.max_len = int(batch), int(total_tokens), int(max_len)
+        n = C.lib().cora_forward_host_workspace_bytes(ctypes.byref(self.cp), self.batch, self.total_tokens, self.max_len)
+        if n == 0:
+            raise C.CoraError(C.CORA_ERR_INVALID, "cora_forward_host_workspace_bytes")
+        self.ws = torch.empty(n, dtype=torch.uint8, device=device)
+        self.layout = C.Layout()
+
+    def __call__(self, lengths_host: torch.Tensor, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> None:
+        for t in (lengths_host, x_host, y_host):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("HostForward takes contiguous host tensors (pinned for async copies)")
+        C.check(C.lib().cora_encoder_forward_host(ctypes.byref(self.cp), _ptr(lengths_host), self.batch,
+                                                  self.total_tokens, self.max_len, _ptr(x_host), _ptr(y_host),
+                                                  _ptr(self.ws), self.ws.numel(), ctypes.byref(self.layout),
+                                                  _stream(stream)), "cora_encoder_forward_host")
+
+    def status(self, stream=None) -> int:
+        return C.lib().cora_layout_status(ctypes.byref(self.layout), _stream(stream))
 
 
 def encoder_layer(x: torch.Tensor, layout: RaggedLayout, params: EncoderParams, out=None, stream=None) -> torch.Tensor:

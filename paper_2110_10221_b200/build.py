@@ -1,9 +1,9 @@
 """Build libcora_b200.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery).
 
-    python -m paper_2110_10221_b200.build [--force]
+    python paper_2110_10221_b200/build.py [--force] [-v]
 
-The shared library exports the C ABI of include/cora.h.  It links the CUDA runtime
-statically and resolves cuTensorMapEncodeTiled through cudaGetDriverEntryPoint, so it has
+The shared library exports the C ABI of include/cora.h.  It links the shared CUDA runtime
+(libcudart.so.12, the one torch already loaded when called from Python) and resolves cuTensorMapEncodeTiled through cudaGetDriverEntryPoint, so it has
 no link-time dependency on libcuda or on torch.
 """
 from __future__ import annotations
@@ -58,7 +58,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     tmp = LIB + ".tmp"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])
+    # Shared cudart: when torch is already loaded, libcudart.so.12 resolves to torch's copy, so the
+    # library and the caller share ONE runtime instance (streams and events interoperate).  The
+    # rpath falls back to the toolkit's copy for plain C callers.
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "shared",
+                           "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     os.replace(tmp, LIB)
     return LIB
 

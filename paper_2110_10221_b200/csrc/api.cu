@@ -226,8 +226,8 @@ cora_status_t cora_layernorm_fwd(const void* x, const void* residual, const floa
   return cuda_status(launch_layernorm(x, residual, gamma, beta, y, rows, cols, eps, dt, as_stream(stream)));
 }
 
-cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
-                                     void* y, void* ws, size_t ws_bytes, void* stream) {
+cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
+                                        void* y, void* ws, size_t ws_bytes, void* stream, void* const* events) {
   if (p == nullptr || layout == nullptr) return CORA_ERR_INVALID;
   const int32_t d = p->d_model, H = p->heads, ff = p->d_ff, T = layout->total_tokens;
   if (d <= 0 || H <= 0 || ff <= 0 || (d % H) != 0 || (d % 8) != 0 || (ff % 8) != 0 || H != layout->heads)
@@ -251,30 +251,89 @@ cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_
   void* f = w + c.f;
   void* y2 = w + c.y2;
   cudaStream_t s = as_stream(stream);
+  auto mark = [&](int k) {
+    if (events != nullptr) cudaEventRecord(static_cast<cudaEvent_t>(events[k]), s);
+  };
   cudaError_t e;
   // a2: QKV = x W_qkv^T + b_qkv
+  mark(0);
   if ((e = launch_gemm(GemmArgs{x, p->w_qkv, p->b_qkv, nullptr, qkv, T, 3 * d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
     return cuda_status(e);
   // a3: fused ragged attention
+  mark(1);
   if ((e = launch_attention(*layout, qkv, o, hd, 1.0f / sqrtf(static_cast<float>(hd)), s)) != cudaSuccess)
     return cuda_status(e);
   // a4: Y1 = O W_o^T + b_o + x
+  mark(2);
   if ((e = launch_gemm(GemmArgs{o, p->w_o, p->b_o, x, y1, T, d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
     return cuda_status(e);
   // a5: H1 = LN1(Y1)
+  mark(3);
   if ((e = launch_layernorm(y1, nullptr, static_cast<const float*>(p->ln1_g), static_cast<const float*>(p->ln1_b), h1,
                             T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
     return cuda_status(e);
   // a6: F = act(H1 W1^T + b1)
+  mark(4);
   if ((e = launch_gemm(GemmArgs{h1, p->w1, p->b1, nullptr, f, T, ff, d, p->act}, s)) != cudaSuccess)
     return cuda_status(e);
   // a7: Y2 = F W2^T + b2 + H1
+  mark(5);
   if ((e = launch_gemm(GemmArgs{f, p->w2, p->b2, h1, y2, T, d, ff, CORA_ACT_NONE}, s)) != cudaSuccess)
     return cuda_status(e);
   // a8: y = LN2(Y2)
+  mark(6);
   if ((e = launch_layernorm(y2, nullptr, static_cast<const float*>(p->ln2_g), static_cast<const float*>(p->ln2_b), y,
                             T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
     return cuda_status(e);
+  mark(7);
+  return CORA_OK;
+}
+
+cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
+                                     void* y, void* ws, size_t ws_bytes, void* stream) {
+  return cora_encoder_layer_fwd_ex(p, layout, x, y, ws, ws_bytes, stream, nullptr);
+}
+
+size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
+                                         int32_t max_len) {
+  if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return 0;
+  const size_t xy = align_up(2ull * static_cast<size_t>(total_tokens) * p->d_model);
+  return align_up(sizeof(int32_t) * (batch + 1)) + 2 * xy +
+         cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len) + carve_encoder(p, total_tokens).total;
+}
+
+cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
+                                        int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host,
+                                        void* ws, size_t ws_bytes, cora_layout_t* layout_out, void* stream) {
+  if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return CORA_ERR_INVALID;
+  if ((batch > 0 && lengths_host == nullptr) || ws == nullptr || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
+    return CORA_ERR_INVALID;
+  if (total_tokens > 0 && (x_host == nullptr || y_host == nullptr)) return CORA_ERR_INVALID;
+  const size_t need = cora_forward_host_workspace_bytes(p, batch, total_tokens, max_len);
+  if (need == 0 || ws_bytes < need) return CORA_ERR_INVALID;
+  const size_t xbytes = 2ull * static_cast<size_t>(total_tokens) * p->d_model;
+  const size_t xy = align_up(xbytes);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int32_t* d_len = reinterpret_cast<int32_t*>(w);
+  w += align_up(sizeof(int32_t) * (batch + 1));
+  void* d_x = w;
+  w += xy;
+  void* d_y = w;
+  w += xy;
+  const size_t lay_bytes = cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len);
+  void* lay_ws = w;
+  w += lay_bytes;
+  cudaStream_t s = as_stream(stream);
+  if (batch > 0 && cudaMemcpyAsync(d_len, lengths_host, sizeof(int32_t) * batch, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return CORA_ERR_CUDA;
+  if (xbytes > 0 && cudaMemcpyAsync(d_x, x_host, xbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return CORA_ERR_CUDA;
+  cora_layout_t L;
+  cora_status_t st = cora_layout_build(d_len, batch, total_tokens, p->heads, max_len, lay_ws, lay_bytes, &L, stream);
+  if (st != CORA_OK) return st;
+  if (layout_out != nullptr) *layout_out = L;
+  st = cora_encoder_layer_fwd_ex(p, &L, d_x, d_y, w, ws_bytes - (w - static_cast<uint8_t*>(ws)), stream, nullptr);
+  if (st != CORA_OK) return st;
+  if (xbytes > 0 && cudaMemcpyAsync(y_host, d_y, xbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CORA_ERR_CUDA;
   return CORA_OK;
 }
 

@@ -60,59 +60,84 @@ struct Vec<__nv_bfloat16> {
   }
 };
 
-// One warp per row; NV 16-byte vectors per lane held in registers (cols <= 32 * NV * E).
-template <typename T, int NV>
-__global__ void __launch_bounds__(256) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ res,
-                                                        const float* __restrict__ gamma,
-                                                        const float* __restrict__ beta, T* __restrict__ y,
-                                                        int32_t rows, int32_t cols, float eps) {
+// Persistent warps; NV 16-byte vectors per lane held in registers (cols <= 32 * NV * E).  gamma and
+// beta are staged once per block in shared memory; each warp streams RPW rows per iteration with
+// all loads issued before the reductions (memory-level parallelism for an HBM-bound kernel).
+template <typename T, int NV, int RPW>
+__global__ void __launch_bounds__(256, 4) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ res,
+                                                           const float* __restrict__ gamma,
+                                                           const float* __restrict__ beta, T* __restrict__ y,
+                                                           int32_t rows, int32_t cols, float eps) {
   constexpr int E = Vec<T>::E;
+  extern __shared__ float4 gb_smem[];  // [cols/4] gamma then [cols/4] beta
+  float* sg = reinterpret_cast<float*>(gb_smem);
+  float* sb = sg + cols;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    sg[c] = __ldg(gamma + c);
+    sb[c] = __ldg(beta + c);
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
   const int nvec = cols / E;
-  const size_t rbase = static_cast<size_t>(row) * cols;
-  float v[NV][E];
-  float s = 0.f;
+  const float inv_cols = 1.0f / cols;
+  for (int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW; row0 < rows;
+       row0 += warps_total * RPW) {
+    float v[RPW][NV][E];
 #pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int vi = lane + 32 * j;
-    if (vi < nvec) {
-      Vec<T>::load(x + rbase + vi * E, v[j]);
-      if (res != nullptr) {
-        float r[E];
-        Vec<T>::load(res + rbase + vi * E, r);
+    for (int r = 0; r < RPW; ++r) {
+      const int row = row0 + r;
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[j][e] += r[e];
-      }
+      for (int j = 0; j < NV; ++j) {
+        const int vi = lane + 32 * j;
+        if (row < rows && vi < nvec) {
+          const size_t off = static_cast<size_t>(row) * cols + vi * E;
+          Vec<T>::load(x + off, v[r][j]);
+          if (res != nullptr) {
+            float rr[E];
+            Vec<T>::load(res + off, rr);
 #pragma unroll
-      for (int e = 0; e < E; ++e) s += v[j][e];
-    }
-  }
-  const float mean = warp_sum(s) / cols;
-  float q = 0.f;
+            for (int e = 0; e < E; ++e) v[r][j][e] += rr[e];
+          }
+        } else {
 #pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    if (lane + 32 * j < nvec) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const float dlt = v[j][e] - mean;
-        q += dlt * dlt;
+          for (int e = 0; e < E; ++e) v[r][j][e] = 0.f;
+        }
       }
     }
-  }
-  const float rstd = rsqrtf(warp_sum(q) / cols + eps);
 #pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int vi = lane + 32 * j;
-    if (vi < nvec) {
-      float o[E];
+    for (int r = 0; r < RPW; ++r) {
+      const int row = row0 + r;
+      float s = 0.f;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int c = vi * E + e;
-        o[e] = (v[j][e] - mean) * rstd * __ldg(gamma + c) + __ldg(beta + c);
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int e = 0; e < E; ++e) s += v[r][j][e];
+      const float mean = warp_sum(s) * inv_cols;
+      float q = 0.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (lane + 32 * j < nvec) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const float dlt = v[r][j][e] - mean;
+            q += dlt * dlt;
+          }
+        }
       }
-      Vec<T>::store(y + rbase + vi * E, o);
+      const float rstd = rsqrtf(warp_sum(q) * inv_cols + eps);
+      if (row < rows) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const int vi = lane + 32 * j;
+          if (vi < nvec) {
+            float o[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) o[e] = (v[r][j][e] - mean) * rstd * sg[vi * E + e] + sb[vi * E + e];
+            Vec<T>::store(y + static_cast<size_t>(row) * cols + vi * E, o);
+          }
+        }
+      }
     }
   }
 }
@@ -168,18 +193,24 @@ cudaError_t dispatch_layernorm(const void* x, const void* res, const float* g, c
                                int32_t cols, float eps, cudaStream_t s) {
   constexpr int E = Vec<T>::E;
   const int per_lane = (cols / E + 31) / 32;
-  const dim3 block(256), grid((rows + 7) / 8);
+  const dim3 block(256);
   auto X = static_cast<const T*>(x);
   auto R = static_cast<const T*>(res);
   auto Y = static_cast<T*>(y);
+  constexpr int RPW = 2;
+  // persistent grid: 4 resident 256-thread blocks per SM, never more warps than row groups
+  const int want = (rows + 8 * RPW - 1) / (8 * RPW);
+  const int cap = device_sm_count() * 4;
+  const dim3 grid(want < cap ? want : cap);
+  const size_t smem = 2 * sizeof(float) * cols;
   if (per_lane <= 1)
-    layernorm_kernel<T, 1><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+    layernorm_kernel<T, 1, RPW><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
   else if (per_lane <= 2)
-    layernorm_kernel<T, 2><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+    layernorm_kernel<T, 2, RPW><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
   else if (per_lane <= 4)
-    layernorm_kernel<T, 4><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+    layernorm_kernel<T, 4, RPW><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
   else
-    layernorm_wide_kernel<T><<<grid, block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
+    layernorm_wide_kernel<T><<<dim3((rows + 7) / 8), block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
   return cudaGetLastError();
 }
 

@@ -257,3 +257,20 @@ def test_layer_virtual_ranks_equal_single_gpu():
             if b1 > b0:
                 parts.append(layer(bf16_cuda(x[ro[b0]:ro[b1]]), _layout(lengths[b0:b1], H)).cpu())
         assert torch.equal(torch.cat(parts), y)
+
+
+def test_layer_events_and_user_stream():
+    # per-kernel events (cora_encoder_layer_fwd_ex) and a non-default stream interoperate with torch
+    lengths, d, H, dff = synth.config("C1")
+    w = synth.encoder_weights(d, H, dff)
+    x = bf16_cuda(synth.activations(int(lengths.sum()), d))
+    layer = P().EncoderLayer(P().EncoderParams.from_host(w))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        lay = _layout(lengths, H)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+        y = layer(x, lay, events=ev)
+    s.synchronize()
+    ref = layer(x, _layout(lengths, H))
+    assert torch.equal(y, ref)
+    assert all(ev[i].elapsed_time(ev[i + 1]) >= 0 for i in range(7))
