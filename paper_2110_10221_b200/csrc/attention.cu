@@ -15,10 +15,13 @@
 //                  S_j = Q K_j^T  (M128 N128 K64, fp32 in TMEM cols [0,128))
 //                  O_j = P_j V_j  (M128 N64 K128, V as an MN-major operand, TMEM cols [128,192))
 //   warps 2..5 : softmax / correction / epilogue, one query row per thread (TMEM lane = row):
-//                  online softmax in the exp2 domain, masking keys >= L_b with -inf
-//                  (reading c18), P_j -> bf16 -> swizzled smem (A operand of the PV MMA),
-//                  o = o * alpha + O_j in registers, o / l -> bf16 -> predicated row stores
-//                  (rows >= L_b belong to the next sequence and are never written).
+//                  S_j is read from TMEM in one pass and the buffer released at once (so S_{j+1}
+//                  overlaps the exponentials), online softmax in the exp2 domain with a lazily
+//                  moved reference max, masking keys >= L_b with -inf in the tail tile only
+//                  (reading c18), P_j -> bf16 -> swizzled smem (A operand of the PV MMA);
+//                  O accumulates in TMEM across KV tiles (rescaled in place only when the
+//                  reference max moves); o / l -> bf16 -> predicated row stores (rows >= L_b
+//                  belong to the next sequence and are never written).
 // Rows of a 128-row TMA box that lie past the sequence end are real rows of the next
 // sequence (finite) or TMA zero-fill past T: their keys are masked and their queries discarded.
 // Two CTAs per SM (96 KB smem, 256 TMEM columns each) overlap one CTA's softmax with the other's MMAs.
@@ -38,6 +41,10 @@ constexpr int TK = 128;       // keys per KV tile
 constexpr int KSTAGES = 2;    // K ring depth
 constexpr int kThreads = 192;
 constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
+// Lazy rescaling (reading a3-r1): the running reference max m_ref of a row is only
+// moved when a new score exceeds it by more than kRescaleLog2 (in log2 units), so P <= 2^8 and the
+// O accumulator in TMEM is rescaled rarely.  O / l is unchanged mathematically.
+constexpr float kRescaleLog2 = 8.0f;
 
 struct AttnSmem {
   static constexpr int kOffQ = 0;
@@ -45,7 +52,7 @@ struct AttnSmem {
   static constexpr int kOffV = kOffK + KSTAGES * kTileBytes;
   static constexpr int kOffP = kOffV + kTileBytes;          // two 128x64 sub-tiles (keys 0-63, 64-127)
   static constexpr int kOffBar = kOffP + 2 * kTileBytes;
-  // q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty, s_full, s_empty, p_full, o_full, o_empty
+  // q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty, s_full, s_empty, p_full, pv_done, o_empty
   static constexpr int kNumBars = 2 + 2 * KSTAGES + 2 + 2 + 1 + 2;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes + 1024;
@@ -76,8 +83,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* s_full = v_empty + 1;
   uint64_t* s_empty = s_full + 1;
   uint64_t* p_full = s_empty + 1;
-  uint64_t* o_full = p_full + 1;
-  uint64_t* o_empty = o_full + 1;
+  uint64_t* pv_done = p_full + 1;
+  uint64_t* o_empty = pv_done + 1;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + AttnSmem::kNumBars);
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(s_full, 1);
     mbar_init(s_empty, 4);
     mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
+    mbar_init(pv_done, 1);
     mbar_init(o_empty, 4);
     fence_barrier_init();
   }
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t p_addr = smem_u32(smem + AttnSmem::kOffP);
       uint32_t q_ph = 0, v_ph = 0, k_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
       int ks = 0;
-      auto issue_s = [&](int j, int nkv) {
+      auto issue_s = [&](bool last) {
         mbar_wait(&k_full[ks], k_ph);
         mbar_wait(s_empty, s_ph ^ 1);
         s_ph ^= 1;
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                        make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
         umma_commit(&k_empty[ks]);
         umma_commit(s_full);
-        if (j == nkv - 1) umma_commit(q_empty);
+        if (last) umma_commit(q_empty);
         if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
       };
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
@@ -164,25 +171,27 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int nkv = (L + TK - 1) / TK;
         mbar_wait(q_full, q_ph);
         q_ph ^= 1;
-        issue_s(0, nkv);
+        issue_s(nkv == 1);
         for (int j = 0; j < nkv; ++j) {
-          if (j + 1 < nkv) issue_s(j + 1, nkv);
-          mbar_wait(p_full, p_ph);
+          if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
+          mbar_wait(p_full, p_ph);                  // P_j in smem (and O rescaled if needed)
           p_ph ^= 1;
           mbar_wait(v_full, v_ph);
           v_ph ^= 1;
-          mbar_wait(o_empty, o_ph ^ 1);
-          o_ph ^= 1;
+          if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
+            mbar_wait(o_empty, o_ph ^ 1);
+            o_ph ^= 1;
+          }
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < TK / 16; ++k) {
             // A = P (K-major, keys 64*(k/4).. in sub-tile k/4), B = V (MN-major: 16 key rows per step)
             const uint64_t pd = make_sdesc_sw128(p_addr + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
             const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
-            umma_bf16_ss(tmem_base + kTmemO, pd, vd, idesc_o, k != 0);
+            umma_bf16_ss(tmem_base + kTmemO, pd, vd, idesc_o, (j | k) != 0);
           }
           umma_commit(v_empty);
-          umma_commit(o_full);
+          umma_commit(pv_done);
         }
       }
     }
@@ -192,99 +201,108 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int i = qd * 32 + lane;  // query row within the tile
     const uint32_t t_lane = (qd * 32) << 16;
     const uint32_t p_base = smem_u32(smem + AttnSmem::kOffP);
-    uint32_t s_ph = 0, o_ph = 0;
+    uint32_t s_ph = 0, pv_ph = 0;
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
       int b, h, qt;
       decode_tile(tiles[idx], b, h, qt);
       const int L = lengths[b], r0 = row_off[b];
       const int nkv = (L + TK - 1) / TK;
-      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
-      float o[HD];
-#pragma unroll
-      for (int c = 0; c < HD; ++c) o[c] = 0.f;
-
-      auto accumulate_o = [&](float alpha) {
-        mbar_wait(o_full, o_ph);
-        o_ph ^= 1;
-        tc_fence_after();
-        uint32_t r[32];
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + half * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; ++c) o[half * 32 + c] = o[half * 32 + c] * alpha + __uint_as_float(r[c]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(o_empty);
-      };
+      float m_ref = -INFINITY, l = 0.f;
 
       for (int j = 0; j < nkv; ++j) {
         const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
         mbar_wait(s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
-        // pass 1: row max over the valid keys
+        uint32_t sr[TK];
+#pragma unroll
+        for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
+        tmem_ld_wait();
+        // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty);
+        float* sv = reinterpret_cast<float*>(sr);
         float mx = -INFINITY;
+        if (valid >= TK) {
 #pragma unroll
-        for (int cb = 0; cb < TK / 32; ++cb) {
-          uint32_t r[32];
-          CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, r);
-          tmem_ld_wait();
+          for (int c = 0; c < TK; ++c) mx = fmaxf(mx, sv[c]);
+        } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (cb * 32 + c < valid) mx = fmaxf(mx, __uint_as_float(r[c]));
+          for (int c = 0; c < TK; ++c) {
+            if (c >= valid) sv[c] = -INFINITY;
+            mx = fmaxf(mx, sv[c]);
+          }
         }
-        const float m_new = fmaxf(m, mx * scale_log2);
-        const float alpha = ex2_approx(m - m_new);
-        m = m_new;
-        // P_{j-1} must be consumed (and O_{j-1} folded in) before P_j overwrites the smem tile
-        if (j > 0) accumulate_o(alpha_prev);
-        // pass 2: p = exp2(s*scale_log2 - m), row sum, bf16 P -> swizzled smem
+        mx *= scale_log2;
+        // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
+        const bool bump = mx > m_ref + kRescaleLog2;
+        const float m_new = bump ? mx : m_ref;
+        const float alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
+        m_ref = m_new;
+        // p = exp2(s * scale_log2 - m_ref), row sum in fp32, P packed to bf16 pairs right away (so at
+        // most 128 fp32 scores + 64 packed words are ever live)
         float rs = 0.f;
+        uint32_t pk[TK / 2];
 #pragma unroll
-        for (int cb = 0; cb < TK / 32; ++cb) {
-          uint32_t r[32];
-          CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, r);
-          tmem_ld_wait();
-          float p[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            p[c] = (cb * 32 + c < valid) ? ex2_approx(__uint_as_float(r[c]) * scale_log2 - m) : 0.f;
-            rs += p[c];
-          }
-          const uint32_t sub = p_base + (cb >> 1) * kTileBytes;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint32_t ch = (cb & 1) * 4 + g;
-            st_shared_v4(sub + sw128_offset(i, ch), pack_bf16x2(p[g * 8 + 0], p[g * 8 + 1]),
-                         pack_bf16x2(p[g * 8 + 2], p[g * 8 + 3]), pack_bf16x2(p[g * 8 + 4], p[g * 8 + 5]),
-                         pack_bf16x2(p[g * 8 + 6], p[g * 8 + 7]));
-          }
+        for (int c = 0; c < TK; c += 2) {
+          const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
+          const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
+          rs += p0 + p1;
+          pk[c / 2] = pack_bf16x2(p0, p1);
         }
+        if (j > 0) {  // PV_{j-1} has consumed P_{j-1} (smem) and accumulated into O (TMEM)
+          mbar_wait(pv_done, pv_ph);
+          pv_ph ^= 1;
+          tc_fence_after();
+        }
+        // bf16 P -> swizzled smem (A operand of PV_j): 16 chunks of 16 B per row
+#pragma unroll
+        for (int ch = 0; ch < TK / 8; ++ch) {
+          const uint32_t sub = p_base + (ch >> 3) * kTileBytes;
+          st_shared_v4(sub + sw128_offset(i, ch & 7), pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+        }
+        // rescale the O accumulator in place when some row of this warp moved its reference max
+        if (j > 0 && __any_sync(0xffffffffu, bump)) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t orr[32];
+            const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
+            CORA_TMEM_LD_32X32B_X32(taddr, orr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+            CORA_TMEM_ST_32X32B_X32(taddr, orr);
+          }
+          tmem_st_wait();
+        }
+        l = l * alpha + rs;
         tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(s_empty);
-          mbar_arrive(p_full);
-        }
-        l = l * alpha + rs;
-        alpha_prev = alpha;
+        if (lane == 0) mbar_arrive(p_full);
       }
-      accumulate_o(alpha_prev);
-      // epilogue: normalise and store the valid query rows of this tile
+      // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
+      mbar_wait(pv_done, pv_ph);
+      pv_ph ^= 1;
+      tc_fence_after();
+      uint32_t orr[HD];
+      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
+      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty);
       const int qrow = qt * TQ + i;
       if (qrow < L) {
         const float inv = 1.f / l;
         uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(r0 + qrow) * d_model + h * HD);
 #pragma unroll
-        for (int g = 0; g < HD / 8; ++g)
-          dst[g] = make_uint4(pack_bf16x2(o[g * 8 + 0] * inv, o[g * 8 + 1] * inv),
-                              pack_bf16x2(o[g * 8 + 2] * inv, o[g * 8 + 3] * inv),
-                              pack_bf16x2(o[g * 8 + 4] * inv, o[g * 8 + 5] * inv),
-                              pack_bf16x2(o[g * 8 + 6] * inv, o[g * 8 + 7] * inv));
+        for (int g = 0; g < HD / 8; ++g) {
+          const float* o = reinterpret_cast<const float*>(orr) + g * 8;
+          dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
+                              pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+        }
       }
     }
   }

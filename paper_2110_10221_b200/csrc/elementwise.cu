@@ -69,17 +69,22 @@ __global__ void __launch_bounds__(256, 4) layernorm_kernel(const T* __restrict__
                                                            const float* __restrict__ beta, T* __restrict__ y,
                                                            int32_t rows, int32_t cols, float eps) {
   constexpr int E = Vec<T>::E;
-  extern __shared__ float4 gb_smem[];  // [cols/4] gamma then [cols/4] beta
+  // gamma/beta staged lane-major: element e of lane l's j-th vector at [(j*E + e)*32 + l], so a
+  // warp reading "its" parameter for (j, e) touches 32 consecutive words (no bank conflicts).
+  extern __shared__ float4 gb_smem[];
+  const int nvec = cols / E;
+  const int slots = ((nvec + 31) / 32) * 32 * E;
   float* sg = reinterpret_cast<float*>(gb_smem);
-  float* sb = sg + cols;
+  float* sb = sg + slots;
   for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-    sg[c] = __ldg(gamma + c);
-    sb[c] = __ldg(beta + c);
+    const int vi = c / E, e = c % E;
+    const int idx = ((vi >> 5) * E + e) * 32 + (vi & 31);
+    sg[idx] = __ldg(gamma + c);
+    sb[idx] = __ldg(beta + c);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
-  const int nvec = cols / E;
   const float inv_cols = 1.0f / cols;
   for (int row0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW; row0 < rows;
        row0 += warps_total * RPW) {
@@ -133,7 +138,8 @@ __global__ void __launch_bounds__(256, 4) layernorm_kernel(const T* __restrict__
           if (vi < nvec) {
             float o[E];
 #pragma unroll
-            for (int e = 0; e < E; ++e) o[e] = (v[r][j][e] - mean) * rstd * sg[vi * E + e] + sb[vi * E + e];
+            for (int e = 0; e < E; ++e)
+              o[e] = (v[r][j][e] - mean) * rstd * sg[(j * E + e) * 32 + lane] + sb[(j * E + e) * 32 + lane];
             Vec<T>::store(y + static_cast<size_t>(row) * cols + vi * E, o);
           }
         }
@@ -202,7 +208,7 @@ cudaError_t dispatch_layernorm(const void* x, const void* res, const float* g, c
   const int want = (rows + 8 * RPW - 1) / (8 * RPW);
   const int cap = device_sm_count() * 4;
   const dim3 grid(want < cap ? want : cap);
-  const size_t smem = 2 * sizeof(float) * cols;
+  const size_t smem = 2 * sizeof(float) * (((cols / E + 31) / 32) * 32 * E);
   if (per_lane <= 1)
     layernorm_kernel<T, 1, RPW><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
   else if (per_lane <= 2)
