@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--impl", default="cora", choices=["cora", "reference"])
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
@@ -245,8 +246,13 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(events=None):
+    lay_holder = {}
+
+    def step(events=None, pre_event=None):
+        if pre_event is not None:
+            pre_event.record()
         lay = P.layout_build(len_dev, T_loc, H, 512) if len(loc_len) else None
+        lay_holder["lay"] = lay
         if lay is not None and T_loc:
             layer(x_dev, lay, out=y_dev, events=events)
         elif events is not None:
@@ -268,12 +274,28 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+
+    n_ev = P._lib.LAYER_EVENTS
+    pre_ev = torch.cuda.Event(enable_timing=True, external=True)  # external: a graph node when captured
+    kev = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    for e in [pre_ev] + kev:  # torch creates events lazily: materialise them before capture
+        e.record()
+    torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph:
+        # one CUDA graph per step: prelude (a1) + 7 layer kernels (+ gather); event-record nodes between
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(kev, pre_ev)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        stream = torch.cuda.current_stream()
     if world > 1:
         dist.barrier()
 
-    n_ev = P._lib.LAYER_EVENTS
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kern_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    kern_rec, pre_rec = [], []
     sampler = ClockSampler(local)
     if not args.no_clocks:
         sampler.start()
@@ -286,8 +308,15 @@ def main():
             if not args.no_flush:
                 flush.zero_()
             step_ev[i][0].record(stream)
-            step(kern_ev[i])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(kev, pre_ev)
             step_ev[i][1].record(stream)
+            # per-kernel events are re-recorded by every step: read them before the next one
+            step_ev[i][1].synchronize()
+            kern_rec.append([kev[j].elapsed_time(kev[j + 1]) for j in range(n_ev - 1)])
+            pre_rec.append(pre_ev.elapsed_time(kev[0]))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -296,8 +325,8 @@ def main():
 
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     ms_local = float(np.mean(step_ms))
-    kern_ms = {k: float(np.mean([ev[j].elapsed_time(ev[j + 1]) for ev in kern_ev])) for j, k in enumerate(KERNELS)}
-    prelude_ms = float(np.mean([a.elapsed_time(ev[0]) for (a, _), ev in zip(step_ev, kern_ev)]))
+    kern_ms = {k: float(np.mean([rec[j] for rec in kern_rec])) for j, k in enumerate(KERNELS)}
+    prelude_ms = float(np.mean(pre_rec))
     if world > 1:
         t = torch.tensor([ms_local], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -390,7 +419,8 @@ def main():
                    "sum_L2": int((lengths ** 2).sum()), "max_len": int(lengths.max()), "d_model": d, "heads": H,
                    "d_ff": dff, "parallelism": f"seq-shard{world}" if world > 1 else "single",
                    "l2": "no flush" if args.no_flush else "flushed (256 MB write) between steps",
-                   "step": "prelude(a1) + 7 layer kernels (a2..a8)" + (" + NCCL all-gather" if world > 1 else "")},
+                   "step": "prelude(a1) + 7 layer kernels (a2..a8)" + (" + NCCL all-gather" if world > 1 else ""),
+                   "launch": "eager" if args.no_graph else "CUDA graph replay per step"},
         "frac_of_peak": {"burst": value / peaks["bf16_tflops"], "sustained": value / peaks["bf16_tflops_sustained"],
                          "source": peaks["source"]},
         "padded_over_useful_flops": padded_flops(lengths, d, dff) / total_flops,

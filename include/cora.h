@@ -92,6 +92,7 @@ typedef struct cora_layout {
   int32_t* seq_of_tok;    /* [T]   f_fo: fused token index -> sequence b */
   int32_t* pos_in_seq;    /* [T]   f_fi: fused token index -> position i (f_oif(b,i) = row_off[b]+i) */
   int32_t* tiles;         /* [n_tiles_max] attention work list, longest first */
+  int32_t* tile_seq;      /* [2*n_tiles_max] (row_off[b], L_b) of each work tile (one 8-byte load) */
   int32_t* n_tiles;       /* [1]   number of valid entries of `tiles` (0 if status != 0) */
   int32_t* status;        /* [1]   CORA_STATUS_* bits, 0 = ok */
 } cora_layout_t;

@@ -42,6 +42,7 @@ class Layout(ctypes.Structure):
         ("seq_of_tok", ctypes.c_void_p),
         ("pos_in_seq", ctypes.c_void_p),
         ("tiles", ctypes.c_void_p),
+        ("tile_seq", ctypes.c_void_p),
         ("n_tiles", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
     ]

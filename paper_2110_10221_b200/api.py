@@ -79,6 +79,7 @@ class RaggedLayout:
             "seq_of_tok": self._view(self.c.seq_of_tok, T, torch.int32),
             "pos_in_seq": self._view(self.c.pos_in_seq, T, torch.int32),
             "tiles": self._view(self.c.tiles, self.c.n_tiles_max, torch.int32),
+            "tile_seq": self._view(self.c.tile_seq, 2 * self.c.n_tiles_max, torch.int32),
             "n_tiles": self._view(self.c.n_tiles, 1, torch.int32),
             "status": self._view(self.c.status, 1, torch.int32),
         }

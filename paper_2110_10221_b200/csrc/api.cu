@@ -83,7 +83,7 @@ int64_t tiles_bound(int32_t batch, int32_t total_tokens, int32_t heads, int32_t 
 }
 
 struct LayoutCarve {
-  size_t row_off, attn_off, seq_of_tok, pos_in_seq, tiles, n_tiles, status, total;
+  size_t row_off, attn_off, seq_of_tok, pos_in_seq, tiles, tile_seq, n_tiles, status, total;
 };
 LayoutCarve carve_layout(int32_t batch, int32_t total_tokens, int64_t n_tiles_max) {
   LayoutCarve c;
@@ -98,6 +98,8 @@ LayoutCarve carve_layout(int32_t batch, int32_t total_tokens, int64_t n_tiles_ma
   o = align_up(o + sizeof(int32_t) * static_cast<size_t>(total_tokens));
   c.tiles = o;
   o = align_up(o + sizeof(int32_t) * static_cast<size_t>(n_tiles_max));
+  c.tile_seq = o;
+  o = align_up(o + 2 * sizeof(int32_t) * static_cast<size_t>(n_tiles_max));
   c.n_tiles = o;
   o = align_up(o + sizeof(int32_t));
   c.status = o;
@@ -166,6 +168,7 @@ cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t t
   L.seq_of_tok = reinterpret_cast<int32_t*>(w + c.seq_of_tok);
   L.pos_in_seq = reinterpret_cast<int32_t*>(w + c.pos_in_seq);
   L.tiles = reinterpret_cast<int32_t*>(w + c.tiles);
+  L.tile_seq = reinterpret_cast<int32_t*>(w + c.tile_seq);
   L.n_tiles = reinterpret_cast<int32_t*>(w + c.n_tiles);
   L.status = reinterpret_cast<int32_t*>(w + c.status);
   launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream));
@@ -252,7 +255,8 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   void* y2 = w + c.y2;
   cudaStream_t s = as_stream(stream);
   auto mark = [&](int k) {
-    if (events != nullptr) cudaEventRecord(static_cast<cudaEvent_t>(events[k]), s);
+    // external record: also works inside stream capture (becomes an event-record node of the graph)
+    if (events != nullptr) cudaEventRecordWithFlags(static_cast<cudaEvent_t>(events[k]), s, cudaEventRecordExternal);
   };
   cudaError_t e;
   // a2: QKV = x W_qkv^T + b_qkv

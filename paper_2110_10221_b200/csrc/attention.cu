@@ -60,17 +60,28 @@ struct AttnSmem {
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemS = 0, kTmemO = 128;
 
-__device__ __forceinline__ void decode_tile(int32_t w, int& b, int& h, int& qt) {
-  b = w & 0xFFFF;
-  h = (w >> 16) & 0xFF;
-  qt = (w >> 24) & 0x7F;
+// One work tile: head h, q-tile qt of a sequence starting at packed row r0 with L tokens.
+struct WorkTile {
+  int h, qt, r0, L;
+};
+// Metadata of work tile idx (two independent loads: the tile word and (row_off[b], L_b)).
+__device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* tile_seq, int idx, int n) {
+  WorkTile t{0, 0, 0, 0};
+  if (idx < n) {
+    const int32_t w = __ldg(tiles + idx);
+    const int2 sq = __ldg(tile_seq + idx);
+    t.h = (w >> 16) & 0xFF;
+    t.qt = (w >> 24) & 0x7F;
+    t.r0 = sq.x;
+    t.L = sq.y;
+  }
+  return t;
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
-                         const int32_t* __restrict__ n_tiles_ptr, const int32_t* __restrict__ lengths,
-                         const int32_t* __restrict__ row_off, __nv_bfloat16* __restrict__ out, int32_t d_model,
-                         float scale_log2) {
+                         const int2* __restrict__ tile_seq, const int32_t* __restrict__ n_tiles_ptr,
+                         __nv_bfloat16* __restrict__ out, int32_t d_model, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::kOffBar);
@@ -118,10 +129,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) {
       uint32_t q_ph = 0, v_ph = 0, k_ph = 0;
       int ks = 0;
+      WorkTile nxt = load_tile(tiles, tile_seq, blockIdx.x, n_tiles);
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        int b, h, qt;
-        decode_tile(tiles[idx], b, h, qt);
-        const int L = lengths[b], r0 = row_off[b];
+        const WorkTile cur = nxt;
+        nxt = load_tile(tiles, tile_seq, idx + gridDim.x, n_tiles);
+        const int h = cur.h, qt = cur.qt, L = cur.L, r0 = cur.r0;
         const int nkv = (L + TK - 1) / TK;
         mbar_wait(q_empty, q_ph ^ 1);
         q_ph ^= 1;
@@ -164,11 +176,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (last) umma_commit(q_empty);
         if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
       };
+      WorkTile nxt = load_tile(tiles, tile_seq, blockIdx.x, n_tiles);
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        int b, h, qt;
-        decode_tile(tiles[idx], b, h, qt);
-        const int L = lengths[b];
-        const int nkv = (L + TK - 1) / TK;
+        const WorkTile cur = nxt;
+        nxt = load_tile(tiles, tile_seq, idx + gridDim.x, n_tiles);
+        const int nkv = (cur.L + TK - 1) / TK;
         mbar_wait(q_full, q_ph);
         q_ph ^= 1;
         issue_s(nkv == 1);
@@ -202,11 +214,39 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t t_lane = (qd * 32) << 16;
     const uint32_t p_base = smem_u32(smem + AttnSmem::kOffP);
     uint32_t s_ph = 0, pv_ph = 0;
+    WorkTile nxt = load_tile(tiles, tile_seq, blockIdx.x, n_tiles);
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-      int b, h, qt;
-      decode_tile(tiles[idx], b, h, qt);
-      const int L = lengths[b], r0 = row_off[b];
+      const WorkTile cur = nxt;
+      nxt = load_tile(tiles, tile_seq, idx + gridDim.x, n_tiles);  // prefetch: used next iteration
+      const int L = cur.L;
       const int nkv = (L + TK - 1) / TK;
+      // query rows of this warp that belong to the sequence (warp-uniform skip when none do)
+      if (cur.qt * TQ + static_cast<int>(qd) * 32 >= L) {
+        // none of this warp's 32 query rows belongs to the sequence: keep the barrier protocol,
+        // skip the math (its P rows are stale, its O rows are never stored)
+        for (int j = 0; j < nkv; ++j) {
+          mbar_wait(s_full, s_ph);
+          s_ph ^= 1;
+          tc_fence_after();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty);
+          if (j > 0) {
+            mbar_wait(pv_done, pv_ph);
+            pv_ph ^= 1;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full);
+        }
+        mbar_wait(pv_done, pv_ph);
+        pv_ph ^= 1;
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty);
+        continue;
+      }
+      const bool warp_live = true;
       float m_ref = -INFINITY, l = 0.f;
 
       for (int j = 0; j < nkv; ++j) {
@@ -215,68 +255,80 @@ __global__ void __launch_bounds__(kThreads, 2)
         s_ph ^= 1;
         tc_fence_after();
         uint32_t sr[TK];
+        if (warp_live) {
 #pragma unroll
-        for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
-        tmem_ld_wait();
+          for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
+          tmem_ld_wait();
+        }
         // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty);
         float* sv = reinterpret_cast<float*>(sr);
-        float mx = -INFINITY;
-        if (valid >= TK) {
-#pragma unroll
-          for (int c = 0; c < TK; ++c) mx = fmaxf(mx, sv[c]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < TK; ++c) {
-            if (c >= valid) sv[c] = -INFINITY;
-            mx = fmaxf(mx, sv[c]);
-          }
-        }
-        mx *= scale_log2;
-        // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
-        const bool bump = mx > m_ref + kRescaleLog2;
-        const float m_new = bump ? mx : m_ref;
-        const float alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
-        m_ref = m_new;
-        // p = exp2(s * scale_log2 - m_ref), row sum in fp32, P packed to bf16 pairs right away (so at
-        // most 128 fp32 scores + 64 packed words are ever live)
-        float rs = 0.f;
+        bool bump = false;
+        float alpha = 1.f;
         uint32_t pk[TK / 2];
+        if (warp_live) {
+          // row max over the valid keys (keys >= L_b masked to -inf in the tail tile), 8 chains
+          if (valid < TK) {
 #pragma unroll
-        for (int c = 0; c < TK; c += 2) {
-          const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
-          const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
-          rs += p0 + p1;
-          pk[c / 2] = pack_bf16x2(p0, p1);
+            for (int c = 0; c < TK; ++c)
+              if (c >= valid) sv[c] = -INFINITY;
+          }
+          float m8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
+          // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
+          bump = mx > m_ref + kRescaleLog2;
+          const float m_new = bump ? mx : m_ref;
+          alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
+          m_ref = m_new;
+          // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0), fp32 row sum in 8 chains,
+          // bf16 pairs packed right away
+          float r8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) r8[k] = 0.f;
+#pragma unroll
+          for (int c = 0; c < TK; c += 2) {
+            const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
+            const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
+            r8[(c >> 1) & 7] += p0 + p1;
+            pk[c / 2] = pack_bf16x2(p0, p1);
+          }
+          l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
         }
         if (j > 0) {  // PV_{j-1} has consumed P_{j-1} (smem) and accumulated into O (TMEM)
           mbar_wait(pv_done, pv_ph);
           pv_ph ^= 1;
           tc_fence_after();
         }
-        // bf16 P -> swizzled smem (A operand of PV_j): 16 chunks of 16 B per row
+        if (warp_live) {
+          // bf16 P -> swizzled smem (A operand of PV_j): 16 chunks of 16 B per row
 #pragma unroll
-        for (int ch = 0; ch < TK / 8; ++ch) {
-          const uint32_t sub = p_base + (ch >> 3) * kTileBytes;
-          st_shared_v4(sub + sw128_offset(i, ch & 7), pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
-        }
-        // rescale the O accumulator in place when some row of this warp moved its reference max
-        if (j > 0 && __any_sync(0xffffffffu, bump)) {
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            uint32_t orr[32];
-            const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
-            CORA_TMEM_LD_32X32B_X32(taddr, orr);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-            CORA_TMEM_ST_32X32B_X32(taddr, orr);
+          for (int ch = 0; ch < TK / 8; ++ch) {
+            const uint32_t sub = p_base + (ch >> 3) * kTileBytes;
+            st_shared_v4(sub + sw128_offset(i, ch & 7), pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2],
+                         pk[ch * 4 + 3]);
           }
-          tmem_st_wait();
+          // rescale the O accumulator in place when some row of this warp moved its reference max
+          if (j > 0 && __any_sync(0xffffffffu, bump)) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint32_t orr[32];
+              const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
+              CORA_TMEM_LD_32X32B_X32(taddr, orr);
+              tmem_ld_wait();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+              CORA_TMEM_ST_32X32B_X32(taddr, orr);
+            }
+            tmem_st_wait();
+          }
         }
-        l = l * alpha + rs;
         tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
@@ -287,16 +339,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       pv_ph ^= 1;
       tc_fence_after();
       uint32_t orr[HD];
-      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
-      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
-      tmem_ld_wait();
+      if (warp_live) {
+        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
+        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
+        tmem_ld_wait();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty);
-      const int qrow = qt * TQ + i;
+      const int qrow = cur.qt * TQ + i;
       if (qrow < L) {
         const float inv = 1.f / l;
-        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(r0 + qrow) * d_model + h * HD);
+        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD);
 #pragma unroll
         for (int g = 0; g < HD / 8; ++g) {
           const float* o = reinterpret_cast<const float*>(orr) + g * 8;
@@ -399,7 +453,8 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
     if (grid == 0) return cudaSuccess;
     const float scale_log2 = scale * 1.4426950408889634f;
     attention_fwd_kernel<<<grid, kThreads, AttnSmem::kAlloc, stream>>>(
-        tm, L.tiles, L.n_tiles, L.lengths, L.row_off, static_cast<__nv_bfloat16*>(o), d, scale_log2);
+        tm, L.tiles, reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, static_cast<__nv_bfloat16*>(o), d,
+        scale_log2);
     return cudaGetLastError();
   }
   const int64_t warps = static_cast<int64_t>(L.total_tokens) * L.heads;

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
                                                                    int32_t max_len, int32_t* __restrict__ row_off,
                                                                    int64_t* __restrict__ attn_off,
                                                                    int32_t* __restrict__ tiles,
+                                                                   int32_t* __restrict__ tile_seq,
                                                                    int32_t* __restrict__ n_tiles,
                                                                    int32_t* __restrict__ status) {
   __shared__ int64_t ws64[32];
@@ -135,9 +136,13 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
     if (valid && v > 0) {
       int32_t rank = running[v] + rank_in_warp;
       for (int w = 0; w < wid; ++w) rank += warp_cnt[w][v];
-      int32_t* out = tiles + bucket_base[v] + rank * heads * v;
+      const int32_t first = bucket_base[v] + rank * heads * v;
+      const int2 seq = make_int2(row_off[b], L);
       for (int h = 0; h < heads; ++h)
-        for (int qt = 0; qt < v; ++qt) out[h * v + qt] = b | (h << 16) | (qt << 24);
+        for (int qt = 0; qt < v; ++qt) {
+          tiles[first + h * v + qt] = b | (h << 16) | (qt << 24);
+          reinterpret_cast<int2*>(tile_seq)[first + h * v + qt] = seq;
+        }
     }
     __syncthreads();
     for (int u = tid; u < kMaxBuckets; u += kScanThreads) {
@@ -177,7 +182,7 @@ __global__ void fusion_maps_kernel(const int32_t* __restrict__ row_off, const in
 void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
                          const cora_layout_t& L, cudaStream_t stream) {
   layout_scan_kernel<<<1, kScanThreads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off,
-                                                     L.attn_off, L.tiles, L.n_tiles, L.status);
+                                                     L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.status);
   if (total_tokens > 0) {
     const int threads = 256;
     fusion_maps_kernel<<<(total_tokens + threads - 1) / threads, threads, 0, stream>>>(

@@ -59,6 +59,9 @@ def test_layout_tables_bit_exact(lengths, heads):
     w = tb["tiles"][:n].astype(np.int64)
     got = list(zip((w & 0xFFFF).tolist(), ((w >> 16) & 0xFF).tolist(), ((w >> 24) & 0x7F).tolist()))
     assert got == ref
+    seq = tb["tile_seq"][:2 * n].reshape(-1, 2).tolist()
+    ro = oracle.row_offsets(lengths)
+    assert seq == [[ro[b], lengths[b]] for b, _, _ in ref]
 
 
 @pytest.mark.parametrize("lengths,T,max_len,expect", [
