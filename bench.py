@@ -220,6 +220,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2110_10221_b200 as P
+    from paper_2110_10221_b200.dist import allgather_ragged, shard_rows
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -229,13 +230,11 @@ def main():
     # ---------------------------------------------------------------- workload (synthetic, seeded)
     w = synth.encoder_weights(d, H, dff)
     x_all = synth.activations(int(lengths.sum()), d)
-    ro = np.concatenate([[0], np.cumsum(lengths)])
-    plan = P.shard_plan(list(lengths), d, dff, world)
+    plan, tok_begin = shard_rows(list(lengths), d, dff, world)
     b0, b1 = plan[rank], plan[rank + 1]
     loc_len = lengths[b0:b1]
     T_loc = int(loc_len.sum())
-    tok_begin = [int(ro[plan[r]]) for r in range(world + 1)]
-    x_loc = x_all[ro[b0]:ro[b1]]
+    x_loc = x_all[tok_begin[rank]:tok_begin[rank + 1]]
     params = P.EncoderParams.from_host(w, device=dev)
     layer = P.EncoderLayer(params)
     len_dev = torch.tensor(loc_len, dtype=torch.int32, device=dev)
@@ -259,11 +258,7 @@ def main():
             for e in events:
                 e.record()
         if world > 1:
-            if T_loc:
-                y_full[tok_begin[rank]:tok_begin[rank + 1]].copy_(y_dev)
-            for r in range(world):
-                if tok_begin[r + 1] > tok_begin[r]:
-                    dist.broadcast(y_full[tok_begin[r]:tok_begin[r + 1]], src=r)
+            allgather_ragged(y_full, y_dev, tok_begin, rank, world)
         return lay
 
     # correctness gate on the benchmarked configuration (status word)
