@@ -255,8 +255,14 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   void* y2 = w + c.y2;
   cudaStream_t s = as_stream(stream);
   auto mark = [&](int k) {
-    // external record: also works inside stream capture (becomes an event-record node of the graph)
-    if (events != nullptr) cudaEventRecordWithFlags(static_cast<cudaEvent_t>(events[k]), s, cudaEventRecordExternal);
+    if (events == nullptr) return;
+    // inside stream capture an external record becomes an event-record node of the graph
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+      cudaEventRecordWithFlags(static_cast<cudaEvent_t>(events[k]), s, cudaEventRecordExternal);
+    else
+      cudaEventRecord(static_cast<cudaEvent_t>(events[k]), s);
   };
   cudaError_t e;
   // a2: QKV = x W_qkv^T + b_qkv

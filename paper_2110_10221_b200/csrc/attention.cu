@@ -55,7 +55,7 @@ struct AttnSmem {
   // q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty, s_full, s_empty, p_full, pv_done, o_empty
   static constexpr int kNumBars = 2 + 2 * KSTAGES + 2 + 2 + 1 + 2;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
-  static constexpr int kAlloc = kBytes + 1024;
+  static constexpr int kAlloc = kBytes;
 };
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemS = 0, kTmemO = 128;
@@ -82,8 +82,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
                          const int2* __restrict__ tile_seq, const int32_t* __restrict__ n_tiles_ptr,
                          __nv_bfloat16* __restrict__ out, int32_t d_model, float scale_log2) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::kOffBar);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;

@@ -214,7 +214,7 @@ cudaError_t dispatch_layernorm(const void* x, const void* res, const float* g, c
   else if (per_lane <= 2)
     layernorm_kernel<T, 2, RPW><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
   else if (per_lane <= 4)
-    layernorm_kernel<T, 4, RPW><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
+    layernorm_kernel<T, 4, 1><<<grid, block, smem, s>>>(X, R, g, b, Y, rows, cols, eps);
   else
     layernorm_wide_kernel<T><<<dim3((rows + 7) / 8), block, 0, s>>>(X, R, g, b, Y, rows, cols, eps);
   return cudaGetLastError();

@@ -30,10 +30,11 @@ __device__ T block_exclusive_scan(T v, T* warp_sums, T& total) {
     T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
+  const int nwarps = blockDim.x >> 5;
   if (lane == 31) warp_sums[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    T s = warp_sums[lane];  // 32 warps
+    T s = lane < nwarps ? warp_sums[lane] : T(0);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       T y = __shfl_up_sync(0xffffffffu, s, o);
@@ -66,7 +67,8 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
   __shared__ unsigned long long s_raw_sum;  // sum of the raw (unclamped) lengths, for the T check
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int i = tid; i < kMaxBuckets; i += kScanThreads) {
+  const int nthreads = blockDim.x, nwarps = nthreads >> 5;
+  for (int i = tid; i < kMaxBuckets; i += nthreads) {
     hist[i] = 0;
     running[i] = 0;
   }
@@ -79,16 +81,22 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
   // ---- pass 1: prefix sums (A_1 arrays) + validation + bucket histogram
   int32_t carry32 = 0;
   int64_t carry64 = 0;
-  for (int base = 0; base < batch; base += kScanThreads) {
+  for (int base = 0; base < batch; base += nthreads) {
     const int b = base + tid;
     int32_t L = 0;
     if (b < batch) {
       L = lengths[b];
-      atomicAdd(&s_raw_sum, static_cast<unsigned long long>(static_cast<int64_t>(L)));
       if (L < 0 || L > max_len) {
         s_bad = 1;  // benign race: every writer stores 1
         L = L < 0 ? 0 : max_len;
       }
+    }
+    // raw (unclamped) sum for the T check: warp reduction, one shared atomic per warp
+    {
+      int64_t raw = (b < batch) ? static_cast<int64_t>(lengths[b]) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, o);
+      if (lane == 0 && raw != 0) atomicAdd(&s_raw_sum, static_cast<unsigned long long>(raw));
     }
     int32_t tot32;
     int64_t tot64;
@@ -97,7 +105,11 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
     if (b < batch) {
       row_off[b] = carry32 + ex32;
       attn_off[b] = carry64 + ex64;
-      atomicAdd(&hist[(L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS], 1);
+    }
+    {  // bucket histogram: one shared atomic per distinct bucket per warp
+      const int32_t v = (b < batch) ? (L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS : -1;
+      const uint32_t same = __match_any_sync(0xffffffffu, v);
+      if (v >= 0 && (same & ((1u << lane) - 1u)) == 0) atomicAdd(&hist[v], __popc(same));
     }
     carry32 += tot32;
     carry64 += tot64;
@@ -106,28 +118,39 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
   int32_t st = 0;
   if (s_bad) st |= CORA_STATUS_BAD_LENGTH;
   if (static_cast<int64_t>(s_raw_sum) != total_tokens) st |= CORA_STATUS_SUM_MISMATCH;
-  if (tid == 0) {
-    row_off[batch] = carry32;
-    attn_off[batch] = carry64;
-    *status = st;
-    // bucket bases in descending tile-count order
-    int32_t acc = 0;
-    for (int v = kMaxBuckets - 1; v >= 0; --v) {
-      bucket_base[v] = acc;
-      acc += heads * v * hist[v];
+  if (wid == 0) {
+    // bucket bases in descending tile-count order: exclusive scan of heads*v*hist[v] from v = 128
+    // down to 0, 32 buckets per step
+    int32_t carry = 0;
+    for (int base = 0; base < kMaxBuckets; base += 32) {
+      const int v = kMaxBuckets - 1 - (base + lane);
+      const int32_t x = v >= 0 ? heads * v * hist[v] : 0;
+      int32_t incl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (v >= 0) bucket_base[v] = carry + incl - x;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    *n_tiles = st ? 0 : acc;
+    if (lane == 0) {
+      row_off[batch] = carry32;
+      attn_off[batch] = carry64;
+      *status = st;
+      *n_tiles = st ? 0 : carry;
+    }
   }
   if (st) return;  // data error: empty work list, nothing else is read
   __syncthreads();
 
   // ---- pass 2: stable rank of each sequence inside its bucket -> tile list
-  for (int base = 0; base < batch; base += kScanThreads) {
+  for (int base = 0; base < batch; base += nthreads) {
     const int b = base + tid;
     const bool valid = b < batch;
     const int32_t L = valid ? lengths[b] : 0;
     const int32_t v = valid ? (L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS : -1;
-    for (int i = tid; i < 32 * kMaxBuckets; i += kScanThreads) (&warp_cnt[0][0])[i] = 0;
+    for (int i = tid; i < nwarps * kMaxBuckets; i += nthreads) (&warp_cnt[0][0])[i] = 0;
     __syncthreads();
     const uint32_t same = __match_any_sync(0xffffffffu, v);
     const int rank_in_warp = __popc(same & ((1u << lane) - 1u));
@@ -145,9 +168,9 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
         }
     }
     __syncthreads();
-    for (int u = tid; u < kMaxBuckets; u += kScanThreads) {
+    for (int u = tid; u < kMaxBuckets; u += nthreads) {
       int32_t s = 0;
-      for (int w = 0; w < 32; ++w) s += warp_cnt[w][u];
+      for (int w = 0; w < nwarps; ++w) s += warp_cnt[w][u];
       running[u] += s;
     }
     __syncthreads();
@@ -181,7 +204,10 @@ __global__ void fusion_maps_kernel(const int32_t* __restrict__ row_off, const in
 
 void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
                          const cora_layout_t& L, cudaStream_t stream) {
-  layout_scan_kernel<<<1, kScanThreads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off,
+  // one CTA sized to the batch (>= 1 warp, <= 1024 threads; larger batches loop in chunks)
+  int threads = ((batch + 31) / 32) * 32;
+  threads = threads < 32 ? 32 : (threads > kScanThreads ? kScanThreads : threads);
+  layout_scan_kernel<<<1, threads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off,
                                                      L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.status);
   if (total_tokens > 0) {
     const int threads = 256;

@@ -138,8 +138,8 @@ def test_linear_plain(m, n, k):
 
 @pytest.mark.parametrize("act", ["none", "relu", "gelu"])
 @pytest.mark.parametrize("use_res", [False, True])
-def test_linear_epilogues(act, use_res):
-    m, n, k = 333, 512, 512
+@pytest.mark.parametrize("m,n,k", [(333, 512, 512), (700, 512, 2048), (130, 264, 1024), (50, 48, 16)])
+def test_linear_epilogues(act, use_res, m, n, k):
     a = synth.round_bf16(synth.normal((m, k), 23))
     w = synth.round_bf16(synth.normal((n, k), 24) / math.sqrt(k))
     b = synth.round_bf16(synth.normal((n,), 25))
