@@ -10,21 +10,23 @@
 // longest-first tile list built by the prelude (static stride over the list).  For one work
 // tile (b, h, qt): Q = 128 query rows of sequence b, head h; K_j / V_j = 128-key tiles,
 // j < ceil(L_b / 128).
-//   warp 0     : TMA producer (Q, K ring of 2, V) from QKV[T, 3d] with 128x64 SWIZZLE_128B boxes
+//   warp 0     : TMA producer (Q x2, K ring of 2, V ring of 2) from QKV[T, 3d], 128x64 SWIZZLE_128B boxes
 //   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer
-//                  S_j = Q K_j^T  (M128 N128 K64, fp32 in TMEM cols [0,128))
-//                  O_j = P_j V_j  (M128 N64 K128, V as an MN-major operand, TMEM cols [128,192))
+//                  S_j = Q K_j^T  (M128 N128 K64, SS form, fp32 in TMEM cols [0,128))
+//                  O  += P_j V_j  (M128 N64 K128, TS form: P read from TMEM cols [128,192) as bf16
+//                                  pairs, V an MN-major smem operand; O in TMEM cols [192,256))
 //   warps 2..5 : softmax / correction / epilogue, one query row per thread (TMEM lane = row):
 //                  S_j is read from TMEM in one pass and the buffer released at once (so S_{j+1}
 //                  overlaps the exponentials), online softmax in the exp2 domain with a lazily
 //                  moved reference max, masking keys >= L_b with -inf in the tail tile only
-//                  (reading c18), P_j -> bf16 -> swizzled smem (A operand of the PV MMA);
+//                  (reading c18), P_j -> bf16 pairs -> TMEM (tcgen05.st; A operand of the PV MMA);
 //                  O accumulates in TMEM across KV tiles (rescaled in place only when the
 //                  reference max moves); o / l -> bf16 -> predicated row stores (rows >= L_b
 //                  belong to the next sequence and are never written).
 // Rows of a 128-row TMA box that lie past the sequence end are real rows of the next
 // sequence (finite) or TMA zero-fill past T: their keys are masked and their queries discarded.
 // Two CTAs per SM (96 KB smem, 256 TMEM columns each) overlap one CTA's softmax with the other's MMAs.
+// Nothing of S or P goes through shared memory or HBM.
 #include <cuda_bf16.h>
 
 #include <cstdint>
@@ -38,7 +40,9 @@ namespace {
 constexpr int HD = 64;        // head dim (one SWIZZLE_128B row)
 constexpr int TQ = 128;       // query rows per work tile
 constexpr int TK = 128;       // keys per KV tile
+constexpr int QSTAGES = 2;    // Q double buffer: the next tile's Q streams in under the current tile
 constexpr int KSTAGES = 2;    // K ring depth
+constexpr int VSTAGES = 2;    // V ring depth
 constexpr int kThreads = 192;
 constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
 // Lazy rescaling (reading a3-r1): the running reference max m_ref of a row is only
@@ -48,34 +52,27 @@ constexpr float kRescaleLog2 = 8.0f;
 
 struct AttnSmem {
   static constexpr int kOffQ = 0;
-  static constexpr int kOffK = kOffQ + kTileBytes;
+  static constexpr int kOffK = kOffQ + QSTAGES * kTileBytes;
   static constexpr int kOffV = kOffK + KSTAGES * kTileBytes;
-  static constexpr int kOffP = kOffV + kTileBytes;          // two 128x64 sub-tiles (keys 0-63, 64-127)
-  static constexpr int kOffBar = kOffP + 2 * kTileBytes;
-  // q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty, s_full, s_empty, p_full, pv_done, o_empty
-  static constexpr int kNumBars = 2 + 2 * KSTAGES + 2 + 2 + 1 + 2;
+  static constexpr int kOffBar = kOffV + VSTAGES * kTileBytes;
+  // q_full/empty[QS], k_full/empty[KS], v_full/empty[VS], s_full, s_empty, p_full, pv_done, o_empty
+  static constexpr int kNumBars = 2 * (QSTAGES + KSTAGES + VSTAGES) + 5;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes;
 };
+// TMEM columns: S (fp32, 128) | P (bf16 pairs, 64) | O (fp32, 64)
 constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kTmemS = 0, kTmemO = 128;
+constexpr uint32_t kTmemS = 0, kTmemP = 128, kTmemO = 192;
 
 // One work tile: head h, q-tile qt of a sequence starting at packed row r0 with L tokens.
 struct WorkTile {
   int h, qt, r0, L;
 };
 // Metadata of work tile idx (two independent loads: the tile word and (row_off[b], L_b)).
-__device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* tile_seq, int idx, int n) {
-  WorkTile t{0, 0, 0, 0};
-  if (idx < n) {
-    const int32_t w = __ldg(tiles + idx);
-    const int2 sq = __ldg(tile_seq + idx);
-    t.h = (w >> 16) & 0xFF;
-    t.qt = (w >> 24) & 0x7F;
-    t.r0 = sq.x;
-    t.L = sq.y;
-  }
-  return t;
+__device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* tile_seq, int idx) {
+  const int32_t w = __ldg(tiles + idx);
+  const int2 sq = __ldg(tile_seq + idx);
+  return WorkTile{(w >> 16) & 0xFF, (w >> 24) & 0x7F, sq.x, sq.y};
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -87,13 +84,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::kOffBar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = q_full + QSTAGES;
+  uint64_t* k_full = q_empty + QSTAGES;
   uint64_t* k_empty = k_full + KSTAGES;
   uint64_t* v_full = k_empty + KSTAGES;
-  uint64_t* v_empty = v_full + 1;
-  uint64_t* s_full = v_empty + 1;
+  uint64_t* v_empty = v_full + VSTAGES;
+  uint64_t* s_full = v_empty + VSTAGES;
   uint64_t* s_empty = s_full + 1;
   uint64_t* p_full = s_empty + 1;
   uint64_t* pv_done = p_full + 1;
@@ -105,14 +102,18 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int s = 0; s < QSTAGES; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
     for (int s = 0; s < KSTAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
     }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
+    for (int s = 0; s < VSTAGES; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(s_empty, 4);
     mbar_init(p_full, 4);
@@ -129,27 +130,26 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t q_ph = 0, v_ph = 0, k_ph = 0;
-      int ks = 0;
-      WorkTile nxt = load_tile(tiles, tile_seq, blockIdx.x, n_tiles);
+      int qs = 0, ks = 0, vs = 0;
+      uint32_t q_ph = 0, k_ph = 0, v_ph = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkTile cur = nxt;
-        nxt = load_tile(tiles, tile_seq, idx + gridDim.x, n_tiles);
-        const int h = cur.h, qt = cur.qt, L = cur.L, r0 = cur.r0;
-        const int nkv = (L + TK - 1) / TK;
-        mbar_wait(q_empty, q_ph ^ 1);
-        q_ph ^= 1;
-        mbar_arrive_expect_tx(q_full, kTileBytes);
-        tma_load_2d(smem + AttnSmem::kOffQ, &tm_qkv, q_full, h * HD, r0 + qt * TQ);
+        const WorkTile cur = load_tile(tiles, tile_seq, idx);
+        const int nkv = (cur.L + TK - 1) / TK;
+        mbar_wait(&q_empty[qs], q_ph ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], kTileBytes);
+        tma_load_2d(smem + AttnSmem::kOffQ + qs * kTileBytes, &tm_qkv, &q_full[qs], cur.h * HD, cur.r0 + cur.qt * TQ);
+        if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
         for (int j = 0; j < nkv; ++j) {
           mbar_wait(&k_empty[ks], k_ph ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
-          tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + h * HD, r0 + j * TK);
+          tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
+                      cur.r0 + j * TK);
           if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-          mbar_wait(v_empty, v_ph ^ 1);
-          v_ph ^= 1;
-          mbar_arrive_expect_tx(v_full, kTileBytes);
-          tma_load_2d(smem + AttnSmem::kOffV, &tm_qkv, v_full, 2 * d_model + h * HD, r0 + j * TK);
+          mbar_wait(&v_empty[vs], v_ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
+          tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
+                      cur.r0 + j * TK);
+          if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
         }
       }
     }
@@ -158,55 +158,51 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK);
       constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HD, /*b_mn_major=*/true);
-      const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ);
-      const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV);
-      const uint32_t p_addr = smem_u32(smem + AttnSmem::kOffP);
-      uint32_t q_ph = 0, v_ph = 0, k_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
-      int ks = 0;
-      auto issue_s = [&](bool last) {
-        mbar_wait(&k_full[ks], k_ph);
-        mbar_wait(s_empty, s_ph ^ 1);
-        s_ph ^= 1;
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
-                       make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
-        umma_commit(&k_empty[ks]);
-        umma_commit(s_full);
-        if (last) umma_commit(q_empty);
-        if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-      };
-      WorkTile nxt = load_tile(tiles, tile_seq, blockIdx.x, n_tiles);
+      int qs = 0, ks = 0, vs = 0;
+      uint32_t q_ph = 0, k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkTile cur = nxt;
-        nxt = load_tile(tiles, tile_seq, idx + gridDim.x, n_tiles);
+        const WorkTile cur = load_tile(tiles, tile_seq, idx);
         const int nkv = (cur.L + TK - 1) / TK;
-        mbar_wait(q_full, q_ph);
-        q_ph ^= 1;
+        mbar_wait(&q_full[qs], q_ph);
+        const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
+        auto issue_s = [&](bool last) {
+          mbar_wait(&k_full[ks], k_ph);
+          mbar_wait(s_empty, s_ph ^ 1);
+          s_ph ^= 1;
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
+                         make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
+          umma_commit(&k_empty[ks]);
+          umma_commit(s_full);
+          if (last) umma_commit(&q_empty[qs]);  // Q slot free once the last S of the tile is done
+          if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+        };
         issue_s(nkv == 1);
         for (int j = 0; j < nkv; ++j) {
           if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
-          mbar_wait(p_full, p_ph);                  // P_j in smem (and O rescaled if needed)
+          mbar_wait(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
           p_ph ^= 1;
-          mbar_wait(v_full, v_ph);
-          v_ph ^= 1;
+          mbar_wait(&v_full[vs], v_ph);
           if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
             mbar_wait(o_empty, o_ph ^ 1);
             o_ph ^= 1;
           }
           tc_fence_after();
+          const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV + vs * kTileBytes);
 #pragma unroll
           for (int k = 0; k < TK / 16; ++k) {
-            // A = P (K-major, keys 64*(k/4).. in sub-tile k/4), B = V (MN-major: 16 key rows per step)
-            const uint64_t pd = make_sdesc_sw128(p_addr + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
+            // A = P from TMEM (16 keys = 8 packed columns per step), B = V (MN-major, 16 key rows per step)
             const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
-            umma_bf16_ss(tmem_base + kTmemO, pd, vd, idesc_o, (j | k) != 0);
+            umma_bf16_ts(tmem_base + kTmemO, tmem_base + kTmemP + k * 8, vd, idesc_o, (j | k) != 0);
           }
-          umma_commit(v_empty);
+          umma_commit(&v_empty[vs]);
           umma_commit(pv_done);
+          if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
         }
+        if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
       }
     }
   } else {
@@ -214,15 +210,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t qd = warp & 3;  // TMEM lane quadrant
     const int i = qd * 32 + lane;  // query row within the tile
     const uint32_t t_lane = (qd * 32) << 16;
-    const uint32_t p_base = smem_u32(smem + AttnSmem::kOffP);
     uint32_t s_ph = 0, pv_ph = 0;
-    WorkTile nxt = load_tile(tiles, tile_seq, blockIdx.x, n_tiles);
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-      const WorkTile cur = nxt;
-      nxt = load_tile(tiles, tile_seq, idx + gridDim.x, n_tiles);  // prefetch: used next iteration
+      const WorkTile cur = load_tile(tiles, tile_seq, idx);
       const int L = cur.L;
       const int nkv = (L + TK - 1) / TK;
-      // query rows of this warp that belong to the sequence (warp-uniform skip when none do)
       if (cur.qt * TQ + static_cast<int>(qd) * 32 >= L) {
         // none of this warp's 32 query rows belongs to the sequence: keep the barrier protocol,
         // skip the math (its P rows are stale, its O rows are never stored)
@@ -248,91 +240,75 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) mbar_arrive(o_empty);
         continue;
       }
-      const bool warp_live = true;
       float m_ref = -INFINITY, l = 0.f;
-
       for (int j = 0; j < nkv; ++j) {
         const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
         mbar_wait(s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
         uint32_t sr[TK];
-        if (warp_live) {
 #pragma unroll
-          for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
-          tmem_ld_wait();
-        }
+        for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
+        tmem_ld_wait();
         // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty);
         float* sv = reinterpret_cast<float*>(sr);
-        bool bump = false;
-        float alpha = 1.f;
-        uint32_t pk[TK / 2];
-        if (warp_live) {
-          // row max over the valid keys (keys >= L_b masked to -inf in the tail tile), 8 chains
-          if (valid < TK) {
+        // row max over the valid keys (keys >= L_b masked to -inf in the tail tile)
+        if (valid < TK) {
 #pragma unroll
-            for (int c = 0; c < TK; ++c)
-              if (c >= valid) sv[c] = -INFINITY;
-          }
-          float m8[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
-          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
-          // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
-          bump = mx > m_ref + kRescaleLog2;
-          const float m_new = bump ? mx : m_ref;
-          alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
-          m_ref = m_new;
-          // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0), fp32 row sum in 8 chains,
-          // bf16 pairs packed right away
-          float r8[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) r8[k] = 0.f;
-#pragma unroll
-          for (int c = 0; c < TK; c += 2) {
-            const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
-            const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
-            r8[(c >> 1) & 7] += p0 + p1;
-            pk[c / 2] = pack_bf16x2(p0, p1);
-          }
-          l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
+          for (int c = 0; c < TK; ++c)
+            if (c >= valid) sv[c] = -INFINITY;
         }
-        if (j > 0) {  // PV_{j-1} has consumed P_{j-1} (smem) and accumulated into O (TMEM)
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
+        // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
+        const bool bump = mx > m_ref + kRescaleLog2;
+        const float m_new = bump ? mx : m_ref;
+        const float alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
+        m_ref = m_new;
+        // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0), fp32 row sum in 8 chains,
+        // bf16 pairs packed right away (the A operand layout of the TS MMA: 2 keys per column)
+        float r8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r8[k] = 0.f;
+        uint32_t pk[TK / 2];
+#pragma unroll
+        for (int c = 0; c < TK; c += 2) {
+          const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
+          const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
+          r8[(c >> 1) & 7] += p0 + p1;
+          pk[c / 2] = pack_bf16x2(p0, p1);
+        }
+        l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
+        if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
           mbar_wait(pv_done, pv_ph);
           pv_ph ^= 1;
           tc_fence_after();
         }
-        if (warp_live) {
-          // bf16 P -> swizzled smem (A operand of PV_j): 16 chunks of 16 B per row
+        CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP, pk);
+        CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP + 32, (pk + 32));
+        // rescale the O accumulator in place when some row of this warp moved its reference max
+        if (j > 0 && __any_sync(0xffffffffu, bump)) {
 #pragma unroll
-          for (int ch = 0; ch < TK / 8; ++ch) {
-            const uint32_t sub = p_base + (ch >> 3) * kTileBytes;
-            st_shared_v4(sub + sw128_offset(i, ch & 7), pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2],
-                         pk[ch * 4 + 3]);
-          }
-          // rescale the O accumulator in place when some row of this warp moved its reference max
-          if (j > 0 && __any_sync(0xffffffffu, bump)) {
+          for (int half = 0; half < 2; ++half) {
+            uint32_t orr[32];
+            const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
+            CORA_TMEM_LD_32X32B_X32(taddr, orr);
+            tmem_ld_wait();
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              uint32_t orr[32];
-              const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
-              CORA_TMEM_LD_32X32B_X32(taddr, orr);
-              tmem_ld_wait();
-#pragma unroll
-              for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-              CORA_TMEM_ST_32X32B_X32(taddr, orr);
-            }
-            tmem_st_wait();
+            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+            CORA_TMEM_ST_32X32B_X32(taddr, orr);
           }
         }
+        tmem_st_wait();
         tc_fence_before();
-        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
       }
@@ -341,11 +317,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       pv_ph ^= 1;
       tc_fence_after();
       uint32_t orr[HD];
-      if (warp_live) {
-        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
-        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
-        tmem_ld_wait();
-      }
+      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
+      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty);
