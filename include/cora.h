@@ -95,6 +95,13 @@ typedef struct cora_layout {
   int32_t* tile_seq;      /* [2*n_tiles_max] (row_off[b], L_b) of each work tile (one 8-byte load) */
   int32_t* n_tiles;       /* [1]   number of valid entries of `tiles` (0 if status != 0) */
   int32_t* status;        /* [1]   CORA_STATUS_* bits, 0 = ok */
+  /* Attention work UNITS: pairs of consecutive q-tiles (2 qp, 2 qp + 1) of one (b, h) that share
+   * their K/V tiles; same longest-first order.  Word layout as `tiles` with qt replaced by qp. */
+  int32_t n_units_max;    /* host bound on the unit list length */
+  int32_t _pad2;
+  int32_t* units;         /* [n_units_max] */
+  int32_t* unit_seq;      /* [2*n_units_max] (row_off[b], L_b) of each unit */
+  int32_t* n_units;       /* [1]   number of valid entries of `units` (0 if status != 0) */
 } cora_layout_t;
 
 /* Encoder layer parameters (nn.Linear convention W[out, in], bf16; LayerNorm fp32).

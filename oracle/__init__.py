@@ -35,6 +35,7 @@ from .layout import (  # noqa: F401
     attn_offset,
     attn_total_size,
     tile_list,
+    unit_list,
     n_tiles,
     validate_lengths,
     STATUS_OK,

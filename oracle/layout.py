@@ -112,6 +112,20 @@ def tile_list(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> List[Tu
     return items
 
 
+def unit_list(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> List[Tuple[int, int, int]]:
+    """Attention work units: pairs of consecutive q-tiles of one (sequence, head) that share their
+    K/V tiles, (b, h, qp) for qp < ceil(ceil(L_b/128)/2), same longest-first key as tile_list
+    (reading c15).  Plain definition: enumerate, then sort."""
+    items = []
+    for b, L in enumerate(lengths):
+        npairs = (n_q_tiles(L, tile) + 1) // 2
+        for h in range(heads):
+            for qp in range(npairs):
+                items.append((b, h, qp))
+    items.sort(key=lambda t: (-n_q_tiles(lengths[t[0]], tile), t[0], t[1], t[2]))
+    return items
+
+
 def n_tiles(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> int:
     return heads * sum(n_q_tiles(L, tile) for L in lengths)
 

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcora_b200.so")
+LIB_PATH = os.environ.get("CORA_LIB_PATH") or os.path.join(HERE, "libcora_b200.so")  # override: experiments
 
 CORA_OK, CORA_ERR_INVALID, CORA_ERR_DATA, CORA_ERR_CUDA, CORA_ERR_UNSUPPORTED, CORA_ERR_NCCL = range(6)
 CORA_DT_BF16, CORA_DT_F32 = 0, 1
@@ -45,6 +45,11 @@ class Layout(ctypes.Structure):
         ("tile_seq", ctypes.c_void_p),
         ("n_tiles", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
+        ("n_units_max", ctypes.c_int32),
+        ("_pad2", ctypes.c_int32),
+        ("units", ctypes.c_void_p),
+        ("unit_seq", ctypes.c_void_p),
+        ("n_units", ctypes.c_void_p),
     ]
 
 

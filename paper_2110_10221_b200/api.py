@@ -81,6 +81,9 @@ class RaggedLayout:
             "tiles": self._view(self.c.tiles, self.c.n_tiles_max, torch.int32),
             "tile_seq": self._view(self.c.tile_seq, 2 * self.c.n_tiles_max, torch.int32),
             "n_tiles": self._view(self.c.n_tiles, 1, torch.int32),
+            "units": self._view(self.c.units, self.c.n_units_max, torch.int32),
+            "unit_seq": self._view(self.c.unit_seq, 2 * self.c.n_units_max, torch.int32),
+            "n_units": self._view(self.c.n_units, 1, torch.int32),
             "status": self._view(self.c.status, 1, torch.int32),
         }
 

@@ -37,16 +37,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out=None, objdir=None) -> str:
+    """Compile every csrc/*.cu and link the shared library (extra_flags/out: experiment variants)."""
+    lib = out or LIB
+    if not force and not extra_flags and out is None and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = objdir or os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra_flags, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     failed = False
@@ -57,15 +59,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     # Shared cudart: when torch is already loaded, libcudart.so.12 resolves to torch's copy, so the
     # library and the caller share ONE runtime instance (streams and events interoperate).  The
     # rpath falls back to the toolkit's copy for plain C callers.
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "shared",
                            "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    flags = [a for a in sys.argv[1:] if a.startswith("-D")]
+    out = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, extra_flags=flags, out=out,
+                objdir=os.path.join(HERE, "build_" + os.path.basename(out)) if out else None))

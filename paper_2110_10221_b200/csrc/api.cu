@@ -82,10 +82,16 @@ int64_t tiles_bound(int32_t batch, int32_t total_tokens, int32_t heads, int32_t 
   return heads * (a < b ? a : b);
 }
 
+int64_t units_bound(int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len) {
+  // sum_b ceil(nq_b / 2) <= (sum_b nq_b + B) / 2
+  return heads * ((tiles_bound(batch, total_tokens, 1, max_len) + batch) / 2);
+}
+
 struct LayoutCarve {
-  size_t row_off, attn_off, seq_of_tok, pos_in_seq, tiles, tile_seq, n_tiles, status, total;
+  size_t row_off, attn_off, seq_of_tok, pos_in_seq, tiles, tile_seq, n_tiles, status, units, unit_seq, n_units,
+      total;
 };
-LayoutCarve carve_layout(int32_t batch, int32_t total_tokens, int64_t n_tiles_max) {
+LayoutCarve carve_layout(int32_t batch, int32_t total_tokens, int64_t n_tiles_max, int64_t n_units_max) {
   LayoutCarve c;
   size_t o = 0;
   c.attn_off = o;
@@ -103,6 +109,12 @@ LayoutCarve carve_layout(int32_t batch, int32_t total_tokens, int64_t n_tiles_ma
   c.n_tiles = o;
   o = align_up(o + sizeof(int32_t));
   c.status = o;
+  o = align_up(o + sizeof(int32_t));
+  c.units = o;
+  o = align_up(o + sizeof(int32_t) * static_cast<size_t>(n_units_max));
+  c.unit_seq = o;
+  o = align_up(o + 2 * sizeof(int32_t) * static_cast<size_t>(n_units_max));
+  c.n_units = o;
   o = align_up(o + sizeof(int32_t));
   c.total = o;
   return c;
@@ -142,7 +154,9 @@ extern "C" {
 
 size_t cora_layout_workspace_bytes(int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len) {
   if (!layout_args_ok(batch, total_tokens, heads, max_len)) return 0;
-  return carve_layout(batch, total_tokens, tiles_bound(batch, total_tokens, heads, max_len)).total;
+  return carve_layout(batch, total_tokens, tiles_bound(batch, total_tokens, heads, max_len),
+                      units_bound(batch, total_tokens, heads, max_len))
+      .total;
 }
 
 cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
@@ -150,8 +164,9 @@ cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t t
   if (out == nullptr || !layout_args_ok(batch, total_tokens, heads, max_len)) return CORA_ERR_INVALID;
   if (batch > 0 && lengths == nullptr) return CORA_ERR_INVALID;
   const int64_t ntm = tiles_bound(batch, total_tokens, heads, max_len);
+  const int64_t num = units_bound(batch, total_tokens, heads, max_len);
   if (ntm > INT32_MAX) return CORA_ERR_INVALID;
-  const LayoutCarve c = carve_layout(batch, total_tokens, ntm);
+  const LayoutCarve c = carve_layout(batch, total_tokens, ntm, num);
   if (ws == nullptr || ws_bytes < c.total || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
     return CORA_ERR_INVALID;
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -171,6 +186,10 @@ cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t t
   L.tile_seq = reinterpret_cast<int32_t*>(w + c.tile_seq);
   L.n_tiles = reinterpret_cast<int32_t*>(w + c.n_tiles);
   L.status = reinterpret_cast<int32_t*>(w + c.status);
+  L.n_units_max = static_cast<int32_t>(num);
+  L.units = reinterpret_cast<int32_t*>(w + c.units);
+  L.unit_seq = reinterpret_cast<int32_t*>(w + c.unit_seq);
+  L.n_units = reinterpret_cast<int32_t*>(w + c.n_units);
   launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream));
   *out = L;
   return cuda_status(cudaGetLastError());

@@ -135,17 +135,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
         const WorkTile cur = load_tile(tiles, tile_seq, idx);
         const int nkv = (cur.L + TK - 1) / TK;
-        mbar_wait(&q_empty[qs], q_ph ^ 1);
+        mbar_wait<false>(&q_empty[qs], q_ph ^ 1);
         mbar_arrive_expect_tx(&q_full[qs], kTileBytes);
         tma_load_2d(smem + AttnSmem::kOffQ + qs * kTileBytes, &tm_qkv, &q_full[qs], cur.h * HD, cur.r0 + cur.qt * TQ);
         if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
         for (int j = 0; j < nkv; ++j) {
-          mbar_wait(&k_empty[ks], k_ph ^ 1);
+          mbar_wait<false>(&k_empty[ks], k_ph ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
           tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
                       cur.r0 + j * TK);
           if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-          mbar_wait(&v_empty[vs], v_ph ^ 1);
+          mbar_wait<false>(&v_empty[vs], v_ph ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
           tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
                       cur.r0 + j * TK);
@@ -163,11 +163,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
         const WorkTile cur = load_tile(tiles, tile_seq, idx);
         const int nkv = (cur.L + TK - 1) / TK;
-        mbar_wait(&q_full[qs], q_ph);
+        mbar_wait<false>(&q_full[qs], q_ph);
         const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
         auto issue_s = [&](bool last) {
-          mbar_wait(&k_full[ks], k_ph);
-          mbar_wait(s_empty, s_ph ^ 1);
+          mbar_wait<false>(&k_full[ks], k_ph);
+          mbar_wait<false>(s_empty, s_ph ^ 1);
           s_ph ^= 1;
           tc_fence_after();
           const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
@@ -183,11 +183,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         issue_s(nkv == 1);
         for (int j = 0; j < nkv; ++j) {
           if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
-          mbar_wait(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
+          mbar_wait<false>(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
           p_ph ^= 1;
-          mbar_wait(&v_full[vs], v_ph);
+          mbar_wait<false>(&v_full[vs], v_ph);
           if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
-            mbar_wait(o_empty, o_ph ^ 1);
+            mbar_wait<false>(o_empty, o_ph ^ 1);
             o_ph ^= 1;
           }
           tc_fence_after();
@@ -219,20 +219,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         // none of this warp's 32 query rows belongs to the sequence: keep the barrier protocol,
         // skip the math (its P rows are stale, its O rows are never stored)
         for (int j = 0; j < nkv; ++j) {
-          mbar_wait(s_full, s_ph);
+          mbar_wait<false>(s_full, s_ph);
           s_ph ^= 1;
           tc_fence_after();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_empty);
           if (j > 0) {
-            mbar_wait(pv_done, pv_ph);
+            mbar_wait<false>(pv_done, pv_ph);
             pv_ph ^= 1;
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
         }
-        mbar_wait(pv_done, pv_ph);
+        mbar_wait<false>(pv_done, pv_ph);
         pv_ph ^= 1;
         tc_fence_after();
         tc_fence_before();
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
-        mbar_wait(s_full, s_ph);
+        mbar_wait<false>(s_full, s_ph);
         s_ph ^= 1;
         tc_fence_after();
         uint32_t sr[TK];
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
         if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
-          mbar_wait(pv_done, pv_ph);
+          mbar_wait<false>(pv_done, pv_ph);
           pv_ph ^= 1;
           tc_fence_after();
         }
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) mbar_arrive(p_full);
       }
       // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
-      mbar_wait(pv_done, pv_ph);
+      mbar_wait<false>(pv_done, pv_ph);
       pv_ph ^= 1;
       tc_fence_after();
       uint32_t orr[HD];

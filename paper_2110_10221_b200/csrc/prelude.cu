@@ -56,11 +56,15 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
                                                                    int32_t* __restrict__ tiles,
                                                                    int32_t* __restrict__ tile_seq,
                                                                    int32_t* __restrict__ n_tiles,
+                                                                   int32_t* __restrict__ units,
+                                                                   int32_t* __restrict__ unit_seq,
+                                                                   int32_t* __restrict__ n_units,
                                                                    int32_t* __restrict__ status) {
   __shared__ int64_t ws64[32];
   __shared__ int32_t ws32[32];
   __shared__ int32_t hist[kMaxBuckets];
   __shared__ int32_t bucket_base[kMaxBuckets];
+  __shared__ int32_t unit_base[kMaxBuckets];
   __shared__ int32_t running[kMaxBuckets];
   __shared__ int32_t warp_cnt[32][kMaxBuckets];
   __shared__ int32_t s_bad;
@@ -121,24 +125,29 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
   if (wid == 0) {
     // bucket bases in descending tile-count order: exclusive scan of heads*v*hist[v] from v = 128
     // down to 0, 32 buckets per step
-    int32_t carry = 0;
+    // (units: the same with ceil(v / 2) pairs per (sequence, head))
+    int32_t carry = 0, ucarry = 0;
     for (int base = 0; base < kMaxBuckets; base += 32) {
       const int v = kMaxBuckets - 1 - (base + lane);
       const int32_t x = v >= 0 ? heads * v * hist[v] : 0;
-      int32_t incl = x;
+      const int32_t ux = v >= 0 ? heads * ((v + 1) / 2) * hist[v] : 0;
+      int32_t incl = x, uincl = ux;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        const int32_t uy = __shfl_up_sync(0xffffffffu, uincl, o);
+        if (lane >= o) incl += y, uincl += uy;
       }
-      if (v >= 0) bucket_base[v] = carry + incl - x;
+      if (v >= 0) bucket_base[v] = carry + incl - x, unit_base[v] = ucarry + uincl - ux;
       carry += __shfl_sync(0xffffffffu, incl, 31);
+      ucarry += __shfl_sync(0xffffffffu, uincl, 31);
     }
     if (lane == 0) {
       row_off[batch] = carry32;
       attn_off[batch] = carry64;
       *status = st;
       *n_tiles = st ? 0 : carry;
+      *n_units = st ? 0 : ucarry;
     }
   }
   if (st) return;  // data error: empty work list, nothing else is read
@@ -165,6 +174,13 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
         for (int qt = 0; qt < v; ++qt) {
           tiles[first + h * v + qt] = b | (h << 16) | (qt << 24);
           reinterpret_cast<int2*>(tile_seq)[first + h * v + qt] = seq;
+        }
+      const int32_t np = (v + 1) / 2;
+      const int32_t ufirst = unit_base[v] + rank * heads * np;
+      for (int h = 0; h < heads; ++h)
+        for (int qp = 0; qp < np; ++qp) {
+          units[ufirst + h * np + qp] = b | (h << 16) | (qp << 24);
+          reinterpret_cast<int2*>(unit_seq)[ufirst + h * np + qp] = seq;
         }
     }
     __syncthreads();
@@ -208,7 +224,8 @@ void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_to
   int threads = ((batch + 31) / 32) * 32;
   threads = threads < 32 ? 32 : (threads > kScanThreads ? kScanThreads : threads);
   layout_scan_kernel<<<1, threads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off,
-                                                     L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.status);
+                                                     L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.units, L.unit_seq,
+                                                     L.n_units, L.status);
   if (total_tokens > 0) {
     const int threads = 256;
     fusion_maps_kernel<<<(total_tokens + threads - 1) / threads, threads, 0, stream>>>(

@@ -39,17 +39,29 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Blocking wait for the phase with the given parity.  The suspend-time hint lets the hardware park
-// the warp inside try_wait instead of spinning through the issue slots.
+// Blocking wait for the phase with the given parity.  SLEEP adds a suspend-time hint so the hardware
+// may park the warp inside try_wait instead of spinning through the issue slots (used where the
+// waiting warps would otherwise steal issue bandwidth; the latency-critical attention pipeline spins).
+template <bool SLEEP = true>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
-      "r"(parity), "r"(0x989680)
-      : "memory");
+  if (SLEEP) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+  }
 }
 
 // ---------------------------------------------------------------- TMA

@@ -62,6 +62,12 @@ def test_layout_tables_bit_exact(lengths, heads):
     seq = tb["tile_seq"][:2 * n].reshape(-1, 2).tolist()
     ro = oracle.row_offsets(lengths)
     assert seq == [[ro[b], lengths[b]] for b, _, _ in ref]
+    nu = int(tb["n_units"][0])
+    uref = oracle.unit_list(lengths, heads)
+    assert nu == len(uref) <= lay.c.n_units_max
+    u = tb["units"][:nu].astype(np.int64)
+    assert list(zip((u & 0xFFFF).tolist(), ((u >> 16) & 0xFF).tolist(), ((u >> 24) & 0x7F).tolist())) == uref
+    assert tb["unit_seq"][:2 * nu].reshape(-1, 2).tolist() == [[ro[b], lengths[b]] for b, _, _ in uref]
 
 
 @pytest.mark.parametrize("lengths,T,max_len,expect", [
@@ -77,6 +83,7 @@ def test_layout_status_word(lengths, T, max_len, expect):
     tb = lay.tables()
     assert int(tb["status"][0]) == expect == oracle.validate_lengths(lengths, T, max_len)
     assert int(tb["n_tiles"][0]) == 0  # empty work list: nothing downstream runs
+    assert int(tb["n_units"][0]) == 0
 
 
 # ---------------------------------------------------------------- a5/a8: LayerNorm

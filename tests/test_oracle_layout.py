@@ -128,3 +128,17 @@ def test_synth_configs_match_survey():
                         ("C2-mnli", 1465, 89879)):
         L, *_ = synth.config(name)
         assert int(L.sum()) == T and int((L ** 2).sum()) == S2
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_unit_list_alternative_derivation(seed):
+    rng = np.random.default_rng(100 + seed)
+    L = list(rng.integers(0, 700, size=int(rng.integers(1, 40))))
+    H = int(rng.integers(1, 9))
+    nq = [(x + 127) // 128 for x in L]
+    order = sorted(range(len(L)), key=lambda b: -nq[b])
+    expect = [(b, h, qp) for b in order for h in range(H) for qp in range((nq[b] + 1) // 2)]
+    assert oracle.unit_list(L, H) == expect
+    # every q-tile of the tile list is covered by exactly one unit (qt // 2 == qp)
+    covered = sorted((b, h, qt) for b, h, qp in expect for qt in (2 * qp, 2 * qp + 1) if qt < nq[b])
+    assert covered == sorted(oracle.tile_list(L, H))
