@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "cora_internal.h"
+#include "ptx.cuh"
 
 namespace cora {
 namespace {
@@ -148,6 +149,111 @@ __global__ void __launch_bounds__(256, 4) layernorm_kernel(const T* __restrict__
   }
 }
 
+// Residual-free LayerNorm with bulk-copy staging: a producer warp streams chunks of RC contiguous rows
+// (<= 32 KB) into a 3-stage shared-memory ring with cp.async.bulk (the bytes in flight per SM no longer
+// depend on registers: 2 CTAs x 3 stages x 32 KB); 8 consumer warps normalise the rows straight out of
+// shared memory and write 16-B vectors to global memory.  Lane l owns columns {(l + 32 j) E + e}, so
+// gamma / beta live in registers for the whole kernel.
+constexpr int kLnStages = 3;
+constexpr int kLnChunkBytes = 32 * 1024;
+constexpr int kLnConsumers = 8;
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(32 * (kLnConsumers + 1), 2)
+    layernorm_bulk_kernel(const T* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
+                          T* __restrict__ y, int32_t rows, int32_t cols, int32_t rc, float eps) {
+  constexpr int E = Vec<T>::E;
+  extern __shared__ __align__(128) uint8_t ln_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ln_smem + kLnStages * kLnChunkBytes);
+  uint64_t* empty = full + kLnStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_chunks = (rows + rc - 1) / rc;
+  const size_t row_bytes = static_cast<size_t>(cols) * sizeof(T);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLnStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kLnConsumers);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == kLnConsumers) {
+    // ---- producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        const int r0 = c * rc, nr = min(rc, rows - r0);
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_load(ln_smem + stage * kLnChunkBytes, reinterpret_cast<const uint8_t*>(x) + r0 * row_bytes, bytes,
+                  &full[stage]);
+        if (++stage == kLnStages) stage = 0, phase ^= 1;
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  const int nvec = cols / E;
+  const float inv_cols = 1.0f / cols;
+  float g[NV][E], bt[NV][E];
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int c = (lane + 32 * j) * E + e;
+      g[j][e] = c < cols ? __ldg(gamma + c) : 0.f;
+      bt[j][e] = c < cols ? __ldg(beta + c) : 0.f;
+    }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const int r0 = c * rc, nr = min(rc, rows - r0);
+    mbar_wait(&full[stage], phase);
+    const T* xs = reinterpret_cast<const T*>(ln_smem + stage * kLnChunkBytes);
+    for (int rr = warp; rr < nr; rr += kLnConsumers) {
+      float v[NV][E];
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int vi = lane + 32 * j;
+        if (vi < nvec) {
+          Vec<T>::load(xs + static_cast<size_t>(rr) * cols + vi * E, v[j]);
+#pragma unroll
+          for (int e = 0; e < E; ++e) s += v[j][e];
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[j][e] = 0.f;
+        }
+      }
+      const float mean = warp_sum(s) * inv_cols;
+      float q = 0.f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (lane + 32 * j < nvec) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) q += (v[j][e] - mean) * (v[j][e] - mean);
+        }
+      const float rstd = rsqrtf(warp_sum(q) * inv_cols + eps);
+      T* yr = y + static_cast<size_t>(r0 + rr) * cols;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int vi = lane + 32 * j;
+        if (vi < nvec) {
+          float o[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) o[e] = (v[j][e] - mean) * rstd * g[j][e] + bt[j][e];
+          Vec<T>::store(yr + vi * E, o);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == kLnStages) stage = 0, phase ^= 1;
+  }
+}
+
 // Rows wider than the register budget: three passes over global memory (L1/L2 hits after the first).
 template <typename T>
 __global__ void __launch_bounds__(256) layernorm_wide_kernel(const T* __restrict__ x, const T* __restrict__ res,
@@ -194,11 +300,38 @@ __global__ void __launch_bounds__(256) layernorm_wide_kernel(const T* __restrict
   }
 }
 
+template <typename T, int NV>
+cudaError_t launch_layernorm_bulk(const T* x, const float* g, const float* b, T* y, int32_t rows, int32_t cols,
+                                  float eps, cudaStream_t s) {
+  const int row_bytes = cols * static_cast<int>(sizeof(T));
+  int rc = kLnChunkBytes / row_bytes;  // rows per chunk
+  if (rc > 64) rc = 64;
+  const size_t smem = kLnStages * kLnChunkBytes + 2 * kLnStages * sizeof(uint64_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(layernorm_bulk_kernel<T, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int chunks = (rows + rc - 1) / rc;
+  const int cap = 2 * device_sm_count();
+  layernorm_bulk_kernel<T, NV><<<chunks < cap ? chunks : cap, 32 * (kLnConsumers + 1), smem, s>>>(x, g, b, y, rows,
+                                                                                                 cols, rc, eps);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t dispatch_layernorm(const void* x, const void* res, const float* g, const float* b, void* y, int32_t rows,
                                int32_t cols, float eps, cudaStream_t s) {
   constexpr int E = Vec<T>::E;
   const int per_lane = (cols / E + 31) / 32;
+  const int row_bytes = cols * static_cast<int>(sizeof(T));
+  if (res == nullptr && row_bytes % 16 == 0 && row_bytes <= kLnChunkBytes && per_lane <= 2) {
+    if (per_lane <= 1)
+      return launch_layernorm_bulk<T, 1>(static_cast<const T*>(x), g, b, static_cast<T*>(y), rows, cols, eps, s);
+    return launch_layernorm_bulk<T, 2>(static_cast<const T*>(x), g, b, static_cast<T*>(y), rows, cols, eps, s);
+  }
   const dim3 block(256);
   auto X = static_cast<const T*>(x);
   auto R = static_cast<const T*>(res);

@@ -49,7 +49,7 @@ __device__ T block_exclusive_scan(T v, T* warp_sums, T& total) {
   return warp_prefix + x - v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t* __restrict__ lengths, int32_t batch,
+__device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ lengths, int32_t batch,
                                                                    int32_t total_tokens, int32_t heads,
                                                                    int32_t max_len, int32_t* __restrict__ row_off,
                                                                    int64_t* __restrict__ attn_off,
@@ -193,6 +193,86 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
   }
 }
 
+__global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t* __restrict__ lengths, int32_t batch,
+                                                                   int32_t total_tokens, int32_t heads,
+                                                                   int32_t max_len, int32_t* __restrict__ row_off,
+                                                                   int64_t* __restrict__ attn_off,
+                                                                   int32_t* __restrict__ tiles,
+                                                                   int32_t* __restrict__ tile_seq,
+                                                                   int32_t* __restrict__ n_tiles,
+                                                                   int32_t* __restrict__ units,
+                                                                   int32_t* __restrict__ unit_seq,
+                                                                   int32_t* __restrict__ n_units,
+                                                                   int32_t* __restrict__ status) {
+  layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles, tile_seq, n_tiles, units,
+                    unit_seq, n_units, status);
+}
+
+constexpr int kMergedMaxBatch = 8192;   // merged single-launch prelude: row_off kept in smem per block
+constexpr int kMapTokensPerBlock = 4096;
+
+// One launch for the whole prelude (batch <= kMergedMaxBatch): block 0 runs the scans / tile lists,
+// blocks 1.. build f_fo / f_fi for kMapTokensPerBlock tokens each, recomputing the (tiny) exclusive
+// scan of the lengths in shared memory instead of waiting for block 0.
+__global__ void __launch_bounds__(kScanThreads) layout_merged_kernel(
+    const int32_t* __restrict__ lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
+    int32_t* __restrict__ row_off, int64_t* __restrict__ attn_off, int32_t* __restrict__ tiles,
+    int32_t* __restrict__ tile_seq, int32_t* __restrict__ n_tiles, int32_t* __restrict__ units,
+    int32_t* __restrict__ unit_seq, int32_t* __restrict__ n_units, int32_t* __restrict__ status,
+    int32_t* __restrict__ seq_of_tok, int32_t* __restrict__ pos_in_seq) {
+  if (blockIdx.x == 0) {
+    layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles, tile_seq, n_tiles,
+                      units, unit_seq, n_units, status);
+    return;
+  }
+  extern __shared__ int32_t s_off[];  // [batch + 1] exclusive prefix of the (clamped) lengths
+  __shared__ int32_t ws32[32];
+  __shared__ int32_t s_bad;
+  __shared__ long long s_raw;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_bad = 0, s_raw = 0;
+  __syncthreads();
+  int32_t carry = 0;
+  for (int base = 0; base < batch; base += blockDim.x) {
+    const int b = base + tid;
+    int32_t L = b < batch ? lengths[b] : 0;
+    long long raw = L;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, o);
+    if (lane == 0 && raw != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_raw), static_cast<unsigned long long>(raw));
+    if (L < 0 || L > max_len) {
+      s_bad = 1;
+      L = L < 0 ? 0 : max_len;
+    }
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan<int32_t>(L, ws32, tot);
+    if (b < batch) s_off[b] = carry + ex;
+    carry += tot;
+  }
+  if (tid == 0) s_off[batch] = carry;
+  __syncthreads();
+  const bool bad = s_bad != 0 || s_raw != total_tokens;
+  const int t0 = (blockIdx.x - 1) * kMapTokensPerBlock;
+  const int t1 = min(total_tokens, t0 + kMapTokensPerBlock);
+  for (int t = t0 + tid; t < t1; t += blockDim.x) {
+    if (bad) {
+      seq_of_tok[t] = -1;
+      pos_in_seq[t] = -1;
+      continue;
+    }
+    int lo = 0, hi = batch;  // invariant: s_off[lo] <= t < s_off[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= t)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    seq_of_tok[t] = lo;
+    pos_in_seq[t] = t - s_off[lo];
+  }
+}
+
 // f_fo / f_fi: for token t, b = max{b : row_off[b] <= t} (skips empty sequences), i = t - row_off[b].
 __global__ void fusion_maps_kernel(const int32_t* __restrict__ row_off, const int32_t* __restrict__ status,
                                    int32_t batch, int32_t total_tokens, int32_t* __restrict__ seq_of_tok,
@@ -220,16 +300,24 @@ __global__ void fusion_maps_kernel(const int32_t* __restrict__ row_off, const in
 
 void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
                          const cora_layout_t& L, cudaStream_t stream) {
-  // one CTA sized to the batch (>= 1 warp, <= 1024 threads; larger batches loop in chunks)
+  // one CTA of the scan sized to the batch (>= 1 warp, <= 1024 threads; larger batches loop in chunks)
   int threads = ((batch + 31) / 32) * 32;
   threads = threads < 32 ? 32 : (threads > kScanThreads ? kScanThreads : threads);
-  layout_scan_kernel<<<1, threads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off,
-                                                     L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.units, L.unit_seq,
-                                                     L.n_units, L.status);
+  if (batch <= kMergedMaxBatch) {
+    if (threads < 256) threads = 256;  // the map blocks share the block size
+    const int map_blocks = (total_tokens + kMapTokensPerBlock - 1) / kMapTokensPerBlock;
+    layout_merged_kernel<<<1 + map_blocks, threads, sizeof(int32_t) * (batch + 1), stream>>>(
+        lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.units,
+        L.unit_seq, L.n_units, L.status, L.seq_of_tok, L.pos_in_seq);
+    return;
+  }
+  layout_scan_kernel<<<1, threads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off,
+                                                L.tiles, L.tile_seq, L.n_tiles, L.units, L.unit_seq, L.n_units,
+                                                L.status);
   if (total_tokens > 0) {
-    const int threads = 256;
-    fusion_maps_kernel<<<(total_tokens + threads - 1) / threads, threads, 0, stream>>>(
-        L.row_off, L.status, batch, total_tokens, L.seq_of_tok, L.pos_in_seq);
+    const int mt = 256;
+    fusion_maps_kernel<<<(total_tokens + mt - 1) / mt, mt, 0, stream>>>(L.row_off, L.status, batch, total_tokens,
+                                                                         L.seq_of_tok, L.pos_in_seq);
   }
 }
 
