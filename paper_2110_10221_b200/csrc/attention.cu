@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + AttnSmem::kNumBars);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int n_tiles = *n_tiles_ptr;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
@@ -126,6 +125,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
+  pdl_wait();  // QKV (previous kernel) complete and visible
+  pdl_trigger();
+  const int n_tiles = *n_tiles_ptr;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -428,10 +430,9 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
     const int grid = L.n_tiles_max < max_grid ? L.n_tiles_max : max_grid;
     if (grid == 0) return cudaSuccess;
     const float scale_log2 = scale * 1.4426950408889634f;
-    attention_fwd_kernel<<<grid, kThreads, AttnSmem::kAlloc, stream>>>(
-        tm, L.tiles, reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, static_cast<__nv_bfloat16*>(o), d,
-        scale_log2);
-    return cudaGetLastError();
+    return launch_pdl(attention_fwd_kernel, dim3(grid), dim3(kThreads), AttnSmem::kAlloc, stream, 1, tm, L.tiles,
+                      reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, static_cast<__nv_bfloat16*>(o), d,
+                      scale_log2);
   }
   const int64_t warps = static_cast<int64_t>(L.total_tokens) * L.heads;
   const dim3 block(256), grid(static_cast<unsigned>((warps + 7) / 8));

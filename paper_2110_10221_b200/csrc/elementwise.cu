@@ -158,7 +158,7 @@ constexpr int kLnStages = 3;
 constexpr int kLnChunkBytes = 32 * 1024;
 constexpr int kLnConsumers = 8;
 
-template <typename T, int NV>
+template <typename T, int NV, int RPW>
 __global__ void __launch_bounds__(32 * (kLnConsumers + 1), 2)
     layernorm_bulk_kernel(const T* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
                           T* __restrict__ y, int32_t rows, int32_t cols, int32_t rc, float eps) {
@@ -177,6 +177,8 @@ __global__ void __launch_bounds__(32 * (kLnConsumers + 1), 2)
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();  // the input rows (previous kernel) are complete and visible
+  pdl_trigger();
   if (warp == kLnConsumers) {
     // ---- producer
     if (lane == 0) {
@@ -212,39 +214,60 @@ __global__ void __launch_bounds__(32 * (kLnConsumers + 1), 2)
     const int r0 = c * rc, nr = min(rc, rows - r0);
     mbar_wait(&full[stage], phase);
     const T* xs = reinterpret_cast<const T*>(ln_smem + stage * kLnChunkBytes);
-    for (int rr = warp; rr < nr; rr += kLnConsumers) {
-      float v[NV][E];
-      float s = 0.f;
+    // RPW rows per warp at a time, interleaved so their shuffle reductions overlap
+    for (int rb = warp * RPW; rb < nr; rb += kLnConsumers * RPW) {
+      float v[RPW][NV][E];
+      float s[RPW];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const int vi = lane + 32 * j;
-        if (vi < nvec) {
-          Vec<T>::load(xs + static_cast<size_t>(rr) * cols + vi * E, v[j]);
+      for (int r = 0; r < RPW; ++r) {
+        s[r] = 0.f;
 #pragma unroll
-          for (int e = 0; e < E; ++e) s += v[j][e];
-        } else {
+        for (int j = 0; j < NV; ++j) {
+          const int vi = lane + 32 * j;
+          if (rb + r < nr && vi < nvec) {
+            Vec<T>::load(xs + static_cast<size_t>(rb + r) * cols + vi * E, v[r][j]);
 #pragma unroll
-          for (int e = 0; e < E; ++e) v[j][e] = 0.f;
+            for (int e = 0; e < E; ++e) s[r] += v[r][j][e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[r][j][e] = 0.f;
+          }
         }
       }
-      const float mean = warp_sum(s) * inv_cols;
-      float q = 0.f;
 #pragma unroll
-      for (int j = 0; j < NV; ++j)
-        if (lane + 32 * j < nvec) {
+      for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-          for (int e = 0; e < E; ++e) q += (v[j][e] - mean) * (v[j][e] - mean);
-        }
-      const float rstd = rsqrtf(warp_sum(q) * inv_cols + eps);
-      T* yr = y + static_cast<size_t>(r0 + rr) * cols;
+        for (int r = 0; r < RPW; ++r) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
+      float q[RPW];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const int vi = lane + 32 * j;
-        if (vi < nvec) {
-          float o[E];
+      for (int r = 0; r < RPW; ++r) {
+        s[r] *= inv_cols;  // mean
+        q[r] = 0.f;
 #pragma unroll
-          for (int e = 0; e < E; ++e) o[e] = (v[j][e] - mean) * rstd * g[j][e] + bt[j][e];
-          Vec<T>::store(yr + vi * E, o);
+        for (int j = 0; j < NV; ++j)
+          if (lane + 32 * j < nvec) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) q[r] += (v[r][j][e] - s[r]) * (v[r][j][e] - s[r]);
+          }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) q[r] += __shfl_xor_sync(0xffffffffu, q[r], o);
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        if (rb + r >= nr) break;
+        const float rstd = rsqrtf(q[r] * inv_cols + eps);
+        T* yr = y + static_cast<size_t>(r0 + rb + r) * cols;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const int vi = lane + 32 * j;
+          if (vi < nvec) {
+            float o[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) o[e] = (v[r][j][e] - s[r]) * rstd * g[j][e] + bt[j][e];
+            Vec<T>::store(yr + vi * E, o);
+          }
         }
       }
     }
@@ -300,7 +323,7 @@ __global__ void __launch_bounds__(256) layernorm_wide_kernel(const T* __restrict
   }
 }
 
-template <typename T, int NV>
+template <typename T, int NV, int RPW = (NV == 1 ? 4 : 2)>
 cudaError_t launch_layernorm_bulk(const T* x, const float* g, const float* b, T* y, int32_t rows, int32_t cols,
                                   float eps, cudaStream_t s) {
   const int row_bytes = cols * static_cast<int>(sizeof(T));
@@ -309,16 +332,15 @@ cudaError_t launch_layernorm_bulk(const T* x, const float* g, const float* b, T*
   const size_t smem = kLnStages * kLnChunkBytes + 2 * kLnStages * sizeof(uint64_t);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(layernorm_bulk_kernel<T, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(layernorm_bulk_kernel<T, NV, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int chunks = (rows + rc - 1) / rc;
   const int cap = 2 * device_sm_count();
-  layernorm_bulk_kernel<T, NV><<<chunks < cap ? chunks : cap, 32 * (kLnConsumers + 1), smem, s>>>(x, g, b, y, rows,
-                                                                                                 cols, rc, eps);
-  return cudaGetLastError();
+  return launch_pdl(layernorm_bulk_kernel<T, NV, RPW>, dim3(chunks < cap ? chunks : cap), dim3(32 * (kLnConsumers + 1)),
+                    smem, s, 1, x, g, b, y, rows, cols, rc, eps);
 }
 
 template <typename T>

@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
+  pdl_wait();  // the previous kernel's outputs (our A / residual) are complete and visible
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (every CTA)
@@ -340,20 +342,8 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   const int units = ((m_blocks + CL - 1) / CL) * n_blocks;
   const int max_units = device_sm_count() / CL;
   const int grid = (units < max_units ? units : max_units) * CL;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = S::kAlloc;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tr, static_cast<const __nv_bfloat16*>(g.bias), g.m, g.n, g.k,
-                            g.act);
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), S::kAlloc, stream, CL, ta, tb, tc, tr,
+                    static_cast<const __nv_bfloat16*>(g.bias), g.m, g.n, g.k, g.act);
 }
 
 }  // namespace

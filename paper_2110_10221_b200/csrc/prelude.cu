@@ -13,6 +13,7 @@
 #include <cstdint>
 
 #include "cora_internal.h"
+#include "ptx.cuh"
 
 namespace cora {
 
@@ -220,6 +221,8 @@ __global__ void __launch_bounds__(kScanThreads) layout_merged_kernel(
     int32_t* __restrict__ tile_seq, int32_t* __restrict__ n_tiles, int32_t* __restrict__ units,
     int32_t* __restrict__ unit_seq, int32_t* __restrict__ n_units, int32_t* __restrict__ status,
     int32_t* __restrict__ seq_of_tok, int32_t* __restrict__ pos_in_seq) {
+  pdl_wait();  // the lengths may come from the previous kernel
+  pdl_trigger();
   if (blockIdx.x == 0) {
     layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles, tile_seq, n_tiles,
                       units, unit_seq, n_units, status);
@@ -306,9 +309,9 @@ void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_to
   if (batch <= kMergedMaxBatch) {
     if (threads < 256) threads = 256;  // the map blocks share the block size
     const int map_blocks = (total_tokens + kMapTokensPerBlock - 1) / kMapTokensPerBlock;
-    layout_merged_kernel<<<1 + map_blocks, threads, sizeof(int32_t) * (batch + 1), stream>>>(
-        lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off, L.tiles, L.tile_seq, L.n_tiles, L.units,
-        L.unit_seq, L.n_units, L.status, L.seq_of_tok, L.pos_in_seq);
+    launch_pdl(layout_merged_kernel, dim3(1 + map_blocks), dim3(threads), sizeof(int32_t) * (batch + 1), stream, 1,
+               lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off, L.tiles, L.tile_seq, L.n_tiles,
+               L.units, L.unit_seq, L.n_units, L.status, L.seq_of_tok, L.pos_in_seq);
     return;
   }
   layout_scan_kernel<<<1, threads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off,

@@ -19,12 +19,12 @@ import subprocess
 import sys
 
 # launch order of one layer step (prelude kernels first), see bench.py KERNELS
-STEP_ORDER = ["layout_scan", "fusion_maps", "qkv_gemm", "attention", "out_proj_gemm", "layernorm1", "ff1_gemm",
-              "ff2_gemm", "layernorm2"]
+STEP_ORDER = ["prelude", "qkv_gemm", "attention", "out_proj_gemm", "layernorm1", "ff1_gemm", "ff2_gemm",
+              "layernorm2"]
 
 
 def short(name: str) -> str:
-    for key in ("layout_scan", "fusion_maps", "gemm", "attention_fwd", "attention_simt", "layernorm",
+    for key in ("layout_merged", "layout_scan", "fusion_maps", "gemm", "attention_fwd", "attention_simt", "layernorm",
                 "ragged_softmax", "FillFunctor", "vectorized_elementwise"):
         if key in name:
             return key
@@ -48,7 +48,7 @@ def launches(tag_dir):
     seq = [(short(r[ik]), float(r[iv]) / 1000.0) for r in rows[1:] if len(r) > iv]
     # keep our kernels of the LAST complete step (layout_scan starts a step)
     ours = [(k, t) for k, t in seq if k not in ("FillFunctor", "vectorized_elementwise")]
-    starts = [i for i, (k, _) in enumerate(ours) if k == "layout_scan"]
+    starts = [i for i, (k, _) in enumerate(ours) if k in ("layout_merged", "layout_scan")]
     if not starts:
         return None
     last = ours[starts[-1]:starts[-1] + len(STEP_ORDER)]
