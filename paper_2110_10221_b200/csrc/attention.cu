@@ -41,7 +41,7 @@ constexpr int HD = 64;        // head dim (one SWIZZLE_128B row)
 constexpr int TQ = 128;       // query rows per work tile
 constexpr int TK = 128;       // keys per KV tile
 constexpr int QSTAGES = 2;    // Q double buffer: the next tile's Q streams in under the current tile
-constexpr int KSTAGES = 2;    // K ring depth
+constexpr int KSTAGES = 3;    // K ring depth
 constexpr int VSTAGES = 2;    // V ring depth
 constexpr int kThreads = 192;
 constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
@@ -130,10 +130,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int n_tiles = *n_tiles_ptr;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producers
+    // lane 0 streams Q and K, lane 1 streams V: the two rings are refilled independently, so a V slot
+    // still held by a pending PV never delays the next K load (and vice versa)
     if (lane == 0) {
-      int qs = 0, ks = 0, vs = 0;
-      uint32_t q_ph = 0, k_ph = 0, v_ph = 0;
+      uint32_t q_ph = 0, k_ph = 0;
+      int qs = 0, ks = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
         const WorkTile cur = load_tile(tiles, tile_seq, idx);
         const int nkv = (cur.L + TK - 1) / TK;
@@ -147,6 +149,15 @@ __global__ void __launch_bounds__(kThreads, 2)
           tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
                       cur.r0 + j * TK);
           if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+        }
+      }
+    } else if (lane == 1) {
+      uint32_t v_ph = 0;
+      int vs = 0;
+      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+        const WorkTile cur = load_tile(tiles, tile_seq, idx);
+        const int nkv = (cur.L + TK - 1) / TK;
+        for (int j = 0; j < nkv; ++j) {
           mbar_wait<false>(&v_empty[vs], v_ph ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
           tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
