@@ -390,6 +390,10 @@ def main():
     for k in KERNELS:
         bound, work, unit = kernel_work(k, T, S2, d, dff)
         dur = kern_ms[k] * 1e-3
+        if k.startswith("layernorm") and kern_ms[k] < 1e-3:
+            # LayerNorm fused into the preceding GEMM's epilogue (cora_linear_residual_layernorm_fwd)
+            kernels[k] = {"ms": kern_ms[k], "fused_into": "out_proj_gemm" if k == "layernorm1" else "ff2_gemm"}
+            continue
         if bound == "tensor":
             ach = work / dur / 1e12
             peak = peaks["bf16_tflops_sustained"]
@@ -400,7 +404,7 @@ def main():
             peak = peaks["hbm_gbs"]
             kernels[k] = {"ms": kern_ms[k], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                           "frac": ach / peak}
-    dom = max(KERNELS, key=lambda k: kern_ms[k])
+    dom = max((k for k in KERNELS if "achieved" in kernels[k]), key=lambda k: kern_ms[k])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):

@@ -144,6 +144,8 @@ cora_status_t cora_layout_status(const cora_layout_t* layout, void* stream);
 size_t cora_encoder_workspace_bytes(const cora_encoder_params_t* p, int32_t total_tokens);
 
 /* y[T, d] = EncoderLayer(x[T, d]) over the ragged batch described by `layout` (bf16 in/out).
+ * When d_model == 512 and T > 128 the two "GEMM + bias + residual, LayerNorm" pairs run as single
+ * fused kernels (cora_linear_residual_layernorm_fwd); otherwise as GEMM then LayerNorm kernels.
  * Steps (Table ap_op_times):
  *   QKV = x W_qkv^T + b_qkv                     (tcgen05 GEMM)
  *   O   = ragged MHA(QKV)                       (fused tcgen05 attention, longest-first tiles)
@@ -160,9 +162,10 @@ cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_
 #define CORA_LAYER_EVENTS 8
 
 /* Same as cora_encoder_layer_fwd; when `events` is non-NULL it points to CORA_LAYER_EVENTS
- * cudaEvent_t handles (caller-created) and event k is recorded on `stream` right before kernel k
+ * cudaEvent_t handles (caller-created) and event k is recorded on `stream` right before step k
  * (0 QKV GEMM, 1 attention, 2 out-proj GEMM, 3 LN1, 4 FF1 GEMM, 5 FF2 GEMM, 6 LN2) and event 7
- * after the last one, so the caller can time every kernel of the layer on the launching stream. */
+ * after the last one, so the caller can time every kernel of the layer on the launching stream.
+ * With the fused GEMM + LayerNorm kernels, steps 3 and 6 are empty (events 3 / 4 and 6 / 7 coincide). */
 cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
                                         void* y, void* ws, size_t ws_bytes, void* stream, void* const* events);
 
@@ -187,6 +190,15 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
  * (PAPER.md:598-604, 929-935).  Requires k % 8 == 0, n % 8 == 0, 16-byte aligned pointers. */
 cora_status_t cora_linear_fwd(const void* a, const void* w, const void* bias, const void* residual, void* c,
                               int32_t m, int32_t n, int32_t k, cora_act_t act, void* stream);
+
+/* c[m, n] = LN(act(a w^T + bias) + residual; gamma, beta, eps) with the LayerNorm (post-LN, biased
+ * variance, fp32 statistics of the bf16-rounded pre-LN values, readings
+ * c2/c3) fused into the GEMM epilogue: a 4-CTA cluster (two CTA pairs) owns full rows and exchanges the
+ * row statistics through distributed shared memory.  Requires n == 512 and m > 128 (returns
+ * CORA_ERR_UNSUPPORTED otherwise); residual, gamma, beta non-NULL; bias may be NULL. */
+cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, const void* bias, const void* residual,
+                                                 const float* gamma, const float* beta, float eps, void* c, int32_t m,
+                                                 int32_t n, int32_t k, cora_act_t act, void* stream);
 
 /* o[T, H*d_h] = per sequence, per head softmax(Q_h K_h^T * scale) V_h on qkv[T, 3*H*d_h] (bf16).
  * Only keys j < L_b of the query's own sequence are attended (no padded rows or columns).

@@ -15,6 +15,7 @@ from .api import (  # noqa: F401
     layernorm,
     layout_build,
     linear,
+    linear_residual_layernorm,
     ragged_attention,
     ragged_softmax,
     shard_plan,

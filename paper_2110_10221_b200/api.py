@@ -213,6 +213,20 @@ def linear(a: torch.Tensor, w: torch.Tensor, bias: Optional[torch.Tensor] = None
     return c
 
 
+def linear_residual_layernorm(a: torch.Tensor, w: torch.Tensor, residual: torch.Tensor, gamma: torch.Tensor,
+                              beta: torch.Tensor, bias: Optional[torch.Tensor] = None, eps: float = 1e-5,
+                              act: str = "none", out=None, stream=None) -> torch.Tensor:
+    """c = LN(act(a w^T + bias) + residual) with the LayerNorm fused into the GEMM epilogue (n == 512)."""
+    _need_cuda(a, w, bias, residual, gamma, beta)
+    m, k = a.shape
+    n = w.shape[0]
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=a.device) if out is None else out
+    C.check(C.lib().cora_linear_residual_layernorm_fwd(_ptr(a), _ptr(w), _ptr(bias), _ptr(residual), _ptr(gamma),
+                                                       _ptr(beta), eps, _ptr(c), m, n, k, _ACT[act], _stream(stream)),
+            "cora_linear_residual_layernorm_fwd")
+    return c
+
+
 def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, scale: Optional[float] = None,
                      out=None, stream=None) -> torch.Tensor:
     _need_cuda(qkv)

@@ -221,6 +221,23 @@ cora_status_t cora_linear_fwd(const void* a, const void* w, const void* bias, co
   return cuda_status(launch_gemm(g, as_stream(stream)));
 }
 
+cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, const void* bias, const void* residual,
+                                                 const float* gamma, const float* beta, float eps, void* c, int32_t m,
+                                                 int32_t n, int32_t k, cora_act_t act, void* stream) {
+  if (m < 0 || n <= 0 || k <= 0 || (k % 8) != 0 || act < CORA_ACT_NONE || act > CORA_ACT_GELU_ERF)
+    return CORA_ERR_INVALID;
+  if (m == 0) return CORA_OK;
+  if (a == nullptr || w == nullptr || c == nullptr || residual == nullptr || gamma == nullptr || beta == nullptr ||
+      !aligned16(a) || !aligned16(w) || !aligned16(c) || !aligned16(residual) || (bias != nullptr && !aligned16(bias)))
+    return CORA_ERR_INVALID;
+  GemmArgs g{a, w, bias, residual, c, m, n, k, act};
+  g.ln_gamma = gamma;
+  g.ln_beta = beta;
+  g.ln_eps = eps;
+  if (!gemm_ln_supported(g)) return CORA_ERR_UNSUPPORTED;
+  return cuda_status(launch_gemm_ln(g, as_stream(stream)));
+}
+
 cora_status_t cora_ragged_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o, int32_t head_dim,
                                         float scale, void* stream) {
   if (layout == nullptr || head_dim <= 0 || head_dim > 128 || (head_dim % 2) != 0) return CORA_ERR_INVALID;
@@ -292,28 +309,46 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   mark(1);
   if ((e = launch_attention(*layout, qkv, o, hd, 1.0f / sqrtf(static_cast<float>(hd)), s)) != cudaSuccess)
     return cuda_status(e);
-  // a4: Y1 = O W_o^T + b_o + x
+  // a4 + a5: H1 = LN1(O W_o^T + b_o + x)   (fused when d_model == 512; Y1 never reaches HBM)
   mark(2);
-  if ((e = launch_gemm(GemmArgs{o, p->w_o, p->b_o, x, y1, T, d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
-    return cuda_status(e);
-  // a5: H1 = LN1(Y1)
-  mark(3);
-  if ((e = launch_layernorm(y1, nullptr, static_cast<const float*>(p->ln1_g), static_cast<const float*>(p->ln1_b), h1,
-                            T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
-    return cuda_status(e);
+  GemmArgs g4{o, p->w_o, p->b_o, x, y1, T, d, d, CORA_ACT_NONE};
+  g4.ln_gamma = static_cast<const float*>(p->ln1_g);
+  g4.ln_beta = static_cast<const float*>(p->ln1_b);
+  g4.ln_eps = p->ln_eps;
+  const bool fuse = gemm_ln_supported(g4);
+  if (fuse) {
+    g4.c = h1;
+    if ((e = launch_gemm_ln(g4, s)) != cudaSuccess) return cuda_status(e);
+    mark(3);
+  } else {
+    if ((e = launch_gemm(GemmArgs{o, p->w_o, p->b_o, x, y1, T, d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
+      return cuda_status(e);
+    mark(3);
+    if ((e = launch_layernorm(y1, nullptr, static_cast<const float*>(p->ln1_g), static_cast<const float*>(p->ln1_b),
+                              h1, T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
+      return cuda_status(e);
+  }
   // a6: F = act(H1 W1^T + b1)
   mark(4);
   if ((e = launch_gemm(GemmArgs{h1, p->w1, p->b1, nullptr, f, T, ff, d, p->act}, s)) != cudaSuccess)
     return cuda_status(e);
-  // a7: Y2 = F W2^T + b2 + H1
+  // a7 + a8: y = LN2(F W2^T + b2 + H1)   (fused when d_model == 512; Y2 never reaches HBM)
   mark(5);
-  if ((e = launch_gemm(GemmArgs{f, p->w2, p->b2, h1, y2, T, d, ff, CORA_ACT_NONE}, s)) != cudaSuccess)
-    return cuda_status(e);
-  // a8: y = LN2(Y2)
-  mark(6);
-  if ((e = launch_layernorm(y2, nullptr, static_cast<const float*>(p->ln2_g), static_cast<const float*>(p->ln2_b), y,
-                            T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
-    return cuda_status(e);
+  if (fuse) {
+    GemmArgs g7{f, p->w2, p->b2, h1, y, T, d, ff, CORA_ACT_NONE};
+    g7.ln_gamma = static_cast<const float*>(p->ln2_g);
+    g7.ln_beta = static_cast<const float*>(p->ln2_b);
+    g7.ln_eps = p->ln_eps;
+    if ((e = launch_gemm_ln(g7, s)) != cudaSuccess) return cuda_status(e);
+    mark(6);
+  } else {
+    if ((e = launch_gemm(GemmArgs{f, p->w2, p->b2, h1, y2, T, d, ff, CORA_ACT_NONE}, s)) != cudaSuccess)
+      return cuda_status(e);
+    mark(6);
+    if ((e = launch_layernorm(y2, nullptr, static_cast<const float*>(p->ln2_g), static_cast<const float*>(p->ln2_b), y,
+                              T, d, p->ln_eps, CORA_DT_BF16, s)) != cudaSuccess)
+      return cuda_status(e);
+  }
   mark(7);
   return CORA_OK;
 }

@@ -24,8 +24,13 @@ struct GemmArgs {
   void* c;
   int32_t m, n, k;
   int32_t act;
+  const float* ln_gamma = nullptr;  // launch_gemm_ln: c = LN(act(a b^T + bias) + residual; gamma, beta, eps)
+  const float* ln_beta = nullptr;
+  float ln_eps = 0.f;
 };
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
+bool gemm_ln_supported(const GemmArgs& g);
+cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream);
 
 cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
                              cudaStream_t stream);

@@ -36,21 +36,26 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiRows = 32;                      // rows per epilogue warp
 constexpr int kEpiBufBytes = kEpiRows * BK * 2;   // 4 KB staging buffer (32 rows x 128 B)
 
-template <int BN, int STAGES, int CL>
+template <int BN, int STAGES, int CL, bool LN>
 struct GemmSmem {
   static constexpr int kChunks = BN / BK;             // 64-column epilogue chunks per tile
   static constexpr int kWarpCols = BN / 2;            // columns per epilogue warp
   static constexpr int kBufs = kWarpCols / BK;        // staging buffers per epilogue warp (one per chunk)
   static constexpr int kABytes = BM * BK * 2;         // this CTA's A rows
-  static constexpr int kBBytes = (BN / CL) * BK * 2;  // this CTA's share of the B tile
+  static constexpr int kBBytes = (CL > 1 ? BN / 2 : BN) * BK * 2;  // this CTA's share of the B tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + STAGES * kABytes;
   static constexpr int kOffC = kOffB + STAGES * kBBytes;  // per warp: kBufs staging buffers
   static constexpr int kOffBias = kOffC + kEpiWarps * kBufs * kEpiBufBytes;  // per warp: kWarpCols bf16
-  static constexpr int kOffBar = kOffBias + kEpiWarps * kWarpCols * 2;
-  // full[STAGES], empty[STAGES], tmem_full[2], tmem_empty[2], res[kEpiWarps][kBufs], tmem ptr
-  static constexpr int kNumBars = 2 * STAGES + 4 + kEpiWarps * kBufs;
+  // LN mode: this CTA's column half of gamma / beta (fp32), per-warp row partials and the partner's
+  static constexpr int kOffGamma = kOffBias + kEpiWarps * kWarpCols * 2;
+  static constexpr int kOffBeta = kOffGamma + (LN ? BN * 4 : 0);
+  static constexpr int kOffPart = kOffBeta + (LN ? BN * 4 : 0);  // float2 [2 acc][2 halves][128 rows]
+  static constexpr int kOffRecv = kOffPart + (LN ? 2 * 2 * BM * 8 : 0);  // float2 [2 acc][128 rows]
+  static constexpr int kOffBar = kOffRecv + (LN ? 2 * BM * 8 : 0);
+  // full[STAGES], empty[STAGES], tmem_full[2], tmem_empty[2], res[kEpiWarps][kBufs], xch[2], tmem ptr
+  static constexpr int kNumBars = 2 * STAGES + 4 + kEpiWarps * kBufs + 2;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes;
   static constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -70,13 +75,18 @@ __device__ __forceinline__ float apply_act(float x, int act) {
 // CTA's accumulator, one 4 KB staging buffer per 64-column chunk.  RESIDUAL: the residual chunks are
 // TMA-loaded into the staging buffers at tile start and the output is written over them in place.
 // CL: 1 = one CTA computes a 128 x BN tile (cta_group::1); 2 = a CTA pair computes a 256 x BN tile
-// (cta_group::2), rank r owning rows [128 r, 128 r + 128) of it.
-template <int BN, int STAGES, bool RESIDUAL, int CL>
+// (cta_group::2), pair rank r owning rows [128 r, 128 r + 128) of it; 4 (LN only) = two CTA pairs compute
+// the two BN-column halves of the same 256 rows (N = 2 BN), so every row of the output lives in one
+// cluster and its LayerNorm statistics are combined across the pairs (section "LN epilogue" below).
+template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                         const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_r,
-                        const __nv_bfloat16* __restrict__ bias, int32_t M, int32_t N, int32_t K, int32_t act) {
-  using S = GemmSmem<BN, STAGES, CL>;
+                        const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
+                        const float* __restrict__ ln_beta, float ln_eps, int32_t M, int32_t N, int32_t K,
+                        int32_t act) {
+  using S = GemmSmem<BN, STAGES, CL, LN>;
+  static_assert(!LN || (CL == 4 && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs with a residual");
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -86,21 +96,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = empty + STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
   uint64_t* res_bar = tmem_empty + 2;  // [kEpiWarps][kBufs]
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(res_bar + kEpiWarps * S::kBufs);
+  uint64_t* xch_bar = res_bar + kEpiWarps * S::kBufs;  // [2 acc] partner's row partials landed (LN)
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(xch_bar + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m_blocks = (M + BM - 1) / BM;
   const int n_blocks = (N + BN - 1) / BN;
   const int k_blocks = (K + BK - 1) / BK;
-  // work units: 128-row tiles (CL = 1) or 256-row tile pairs (CL = 2), strided over CTAs / clusters
-  const uint32_t rank = CL > 1 ? cluster_ctarank() : 0u;
-  const bool leader = rank == 0;
-  const int unit0 = CL > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
-  const int unit_step = CL > 1 ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
-  const int num_units = ((m_blocks + CL - 1) / CL) * n_blocks;
-  auto unit_m0 = [&](int u) { return ((u / n_blocks) * CL + static_cast<int>(rank)) * BM; };
-  auto unit_n0 = [&](int u) { return (u % n_blocks) * BN; };
-  constexpr uint16_t kPairMask = (1u << CL) - 1u;
+  // work units: 128-row tiles (CL = 1), 256-row tiles of one BN-column block (CL = 2) or 256 full rows
+  // (CL = 4), strided over CTAs / clusters
+  constexpr bool PAIR = CL > 1;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t prank = PAIR ? (rank & 1u) : 0u;       // rank inside the CTA pair
+  const uint32_t lead_rank = rank & ~1u;                // the pair's leader (issues the MMAs)
+  const int half = LN ? static_cast<int>(rank >> 1) : 0;  // LN: which BN-column half of the rows
+  const bool leader = prank == 0;
+  const int unit0 = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int unit_step = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
+  const int nb_units = LN ? 1 : n_blocks;
+  const int num_units = ((m_blocks + (PAIR ? 1 : 0)) / (PAIR ? 2 : 1)) * nb_units;
+  auto unit_m0 = [&](int u) { return ((u / nb_units) * (PAIR ? 2 : 1) + static_cast<int>(prank)) * BM; };
+  auto unit_n0 = [&](int u) { return LN ? half * BN : (u % nb_units) * BN; };
+  const uint16_t kPairMask = static_cast<uint16_t>(3u << lead_rank);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a);
@@ -114,18 +131,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], kEpiWarps * CL);  // (leader) the epilogue warps of every CTA
+      mbar_init(&tmem_empty[a], kEpiWarps * (PAIR ? 2 : 1));  // (leader) the epilogue warps of both CTAs
+      mbar_init(&xch_bar[a], 1);                               // LN: local arm + the partner's st.async bytes
     }
     fence_barrier_init();
   }
   if (warp == 1) {
-    if (CL > 1)
+    if (PAIR)
       tmem_alloc_cg2<S::kTmemCols>(tmem_ptr);
     else
       tmem_alloc<S::kTmemCols>(tmem_ptr);
   }
   tc_fence_before();
-  if (CL > 1)
+  if (PAIR)
     cluster_sync_all();  // barrier inits visible cluster-wide before any remote complete_tx / arrive
   else
     __syncthreads();
@@ -145,12 +163,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + S::kOffA + stage * S::kABytes;
           uint8_t* sb = smem + S::kOffB + stage * S::kBBytes;
-          if (CL > 1) {
-            // both CTAs' A rows and B halves complete the LEADER's full barrier
-            const uint32_t bar = mapa_shared(&full[stage], 0);
-            if (leader) mbar_arrive_expect_tx(&full[stage], CL * S::kStageBytes);
+          if (PAIR) {
+            // both CTAs' A rows and B halves complete the pair leader's full barrier
+            const uint32_t bar = mapa_shared(&full[stage], lead_rank);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::kStageBytes);
             tma_load_2d_cg2(sa, &tm_a, bar, kb * BK, m0);
-            tma_load_2d_cg2(sb, &tm_b, bar, kb * BK, n0 + static_cast<int>(rank) * (BN / CL));
+            tma_load_2d_cg2(sb, &tm_b, bar, kb * BK, n0 + static_cast<int>(prank) * (BN / 2));
           } else {
             mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
             tma_load_2d(sa, &tm_a, &full[stage], kb * BK, m0);
@@ -163,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader, one thread)
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM * CL, BN);
+      constexpr uint32_t idesc = make_idesc_bf16(BM * (PAIR ? 2 : 1), BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -181,26 +199,152 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = make_sdesc_sw128(b_addr + k * 32, 16, 1024);
-            if (CL > 1)
+            if (PAIR)
               umma_bf16_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
             else
               umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           // frees the smem stage (of every CTA of the pair) once these MMAs retire
-          if (CL > 1)
+          if (PAIR)
             umma_commit_cg2_mcast(&empty[stage], kPairMask);
           else
             umma_commit(&empty[stage]);
           if (++stage == STAGES) stage = 0, phase ^= 1;
         }
         // accumulator ready for the epilogue of every CTA
-        if (CL > 1)
+        if (PAIR)
           umma_commit_cg2_mcast(&tmem_full[acc], kPairMask);
         else
           umma_commit(&tmem_full[acc]);
         if (++acc == 2) acc = 0, acc_phase ^= 1;
       }
     }
+  } else if (LN) {
+    // ------------------------------------------------------------ LN epilogue (every CTA)
+    // Warp (q, hf) owns rows [32 q, 32 q + 32) x columns [hf 128, hf 128 + 128) of this CTA's BN-column
+    // half.  pass 1: v = bf16(acc + bias + residual) into the staging buffers (the rounding point of
+    // the unfused path, Y1 / Y2) and per-row (sum v, sum v^2); the two column quarters of a row are
+    // combined in smem, the CTA partial is sent with st.async to the CTA holding the row's other
+    // column half (rank ^ 2), whose bytes complete this CTA's xch_bar; pass 2: normalise
+    // (v - mean) * rstd * gamma + beta (reading c2/c3: post-LN, biased variance) in place, TMA store.
+    const uint32_t q = warp & 3;
+    const uint32_t ew = warp - 2;
+    const int hf = static_cast<int>(ew) / 4;
+    const int row = static_cast<int>(q) * 32 + static_cast<int>(lane);  // accumulator row of this thread
+    uint8_t* cbuf = smem + S::kOffC + ew * S::kBufs * kEpiBufBytes;
+    uint64_t* rbar = res_bar + ew * S::kBufs;
+    __nv_bfloat16* sbias = reinterpret_cast<__nv_bfloat16*>(smem + S::kOffBias);  // [BN] this CTA's half
+    float* sgamma = reinterpret_cast<float*>(smem + S::kOffGamma);
+    float* sbeta = reinterpret_cast<float*>(smem + S::kOffBeta);
+    float2* part = reinterpret_cast<float2*>(smem + S::kOffPart);  // [acc][hf][row]
+    float2* recv = reinterpret_cast<float2*>(smem + S::kOffRecv);  // [acc][row]
+    const uint32_t tmem_empty_lead0 = mapa_shared(&tmem_empty[0], lead_rank);
+    const uint32_t partner = rank ^ 2u;
+    const uint32_t recv_remote0 = mapa_shared(recv, partner);
+    const uint32_t xch_remote0 = mapa_shared(&xch_bar[0], partner);
+    const int n_half0 = half * BN;
+    // this CTA's column half of bias / gamma / beta, once
+    for (int c = static_cast<int>(threadIdx.x) - 64; c < BN; c += 32 * kEpiWarps) {
+      sbias[c] = bias != nullptr ? bias[n_half0 + c] : __float2bfloat16_rn(0.f);
+      sgamma[c] = ln_gamma[n_half0 + c];
+      sbeta[c] = ln_beta[n_half0 + c];
+    }
+    named_bar_sync(1, 32 * kEpiWarps);
+    const float inv_n = 1.0f / static_cast<float>(N);
+    int acc = 0;
+    uint32_t acc_phase = 0, res_phase = 0;
+    for (int u = unit0; u < num_units; u += unit_step) {
+      const int m0 = unit_m0(u);
+      const int nw = n_half0 + hf * S::kWarpCols;
+      const int row0 = m0 + static_cast<int>(q) * 32;
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) {
+        for (int c = 0; c < S::kBufs; ++c) {
+          mbar_arrive_expect_tx(&rbar[c], kEpiBufBytes);
+          tma_load_2d(cbuf + c * kEpiBufBytes, &tm_r, &rbar[c], nw + c * BK, row0);
+        }
+        if (ew == 0) mbar_arrive_expect_tx(&xch_bar[acc], BM * 8);  // the partner's 128 row partials
+      }
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < S::kBufs; ++c) {
+        uint32_t r[64];
+        const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN + hf * S::kWarpCols + c * BK;
+        CORA_TMEM_LD_32X32B_X32(taddr, r);
+        CORA_TMEM_LD_32X32B_X32(taddr + 32, (r + 32));
+        tmem_ld_wait();
+        if (c == S::kBufs - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_lead0 + acc * 8);
+        }
+        const uint32_t sbase = smem_u32(cbuf + c * kEpiBufBytes);
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(sbias + hf * S::kWarpCols + c * BK);
+        mbar_wait(&rbar[c], (res_phase >> c) & 1u);
+        res_phase ^= 1u << c;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t w[4];
+          ld_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
+          uint32_t o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t b2 = bw[ch * 4 + i];
+            float v0 = __uint_as_float(r[ch * 8 + 2 * i]) + bf16_lo(b2);
+            float v1 = __uint_as_float(r[ch * 8 + 2 * i + 1]) + bf16_hi(b2);
+            if (act != CORA_ACT_NONE) v0 = apply_act(v0, act), v1 = apply_act(v1, act);
+            o[i] = pack_bf16x2(v0 + bf16_lo(w[i]), v1 + bf16_hi(w[i]));
+            const float y0 = bf16_lo(o[i]), y1 = bf16_hi(o[i]);  // statistics of the rounded values
+            s1 += y0 + y1;
+            s2 = fmaf(y0, y0, fmaf(y1, y1, s2));
+          }
+          st_shared_v4(sbase + sw128_offset(lane, ch), o[0], o[1], o[2], o[3]);
+        }
+      }
+      float2* pa = part + acc * 2 * BM;
+      pa[hf * BM + row] = make_float2(s1, s2);
+      named_bar_sync(1, 32 * kEpiWarps);  // both column quarters of every row are in `part`
+      const float2 p0 = pa[row], p1 = pa[BM + row];
+      const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial
+      if (hf == 0)
+        st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
+      mbar_wait(&xch_bar[acc], acc_phase);
+      const float2 pr = recv[acc * BM + row];
+      const float mean = (c1 + pr.x) * inv_n;
+      const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
+      const float rstd = rsqrtf(var + ln_eps);
+#pragma unroll 1
+      for (int c = 0; c < S::kBufs; ++c) {
+        uint8_t* buf = cbuf + c * kEpiBufBytes;
+        const uint32_t sbase = smem_u32(buf);
+        const float* gm = sgamma + hf * S::kWarpCols + c * BK;
+        const float* bt = sbeta + hf * S::kWarpCols + c * BK;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t w[4];
+          ld_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int col = ch * 8 + 2 * i;
+            w[i] = pack_bf16x2((bf16_lo(w[i]) - mean) * rstd * gm[col] + bt[col],
+                               (bf16_hi(w[i]) - mean) * rstd * gm[col + 1] + bt[col + 1]);
+          }
+          st_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tm_c, buf, nw + c * BK, row0);
+          tma_store_commit();
+        }
+      }
+      if (++acc == 2) acc = 0, acc_phase ^= 1;
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue warps (every CTA)
     const uint32_t q = warp & 3;  // TMEM lane quadrant accessible to this warp
@@ -209,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* cbuf = smem + S::kOffC + ew * S::kBufs * kEpiBufBytes;
     __nv_bfloat16* sbias = reinterpret_cast<__nv_bfloat16*>(smem + S::kOffBias + ew * S::kWarpCols * 2);
     uint64_t* rbar = res_bar + ew * S::kBufs;
-    const uint32_t tmem_empty_lead0 = CL > 1 ? mapa_shared(&tmem_empty[0], 0) : 0u;
+    const uint32_t tmem_empty_lead0 = PAIR ? mapa_shared(&tmem_empty[0], lead_rank) : 0u;
     int acc = 0;
     uint32_t acc_phase = 0, res_phase = 0;
     for (int u = unit0; u < num_units; u += unit_step) {
@@ -291,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if (CL > 1)
+            if (PAIR)
               mbar_arrive_cluster(tmem_empty_lead0 + acc * 8);
             else
               mbar_arrive(&tmem_empty[acc]);
@@ -305,24 +449,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  if (CL > 1)
-    cluster_sync_all();  // the peer may still complete_tx / arrive on this CTA's barriers until here
+  if (PAIR)
+    cluster_sync_all();  // the peers may still complete_tx / arrive on this CTA's barriers until here
   else
     __syncthreads();
   if (warp == 1) {
-    if (CL > 1)
+    if (PAIR)
       tmem_dealloc_cg2<S::kTmemCols>(tmem_base);
     else
       tmem_dealloc<S::kTmemCols>(tmem_base);
   }
 }
 
-template <int BN, int STAGES, bool RESIDUAL, int CL>
+template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false>
 cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
-  using S = GemmSmem<BN, STAGES, CL>;
+  using S = GemmSmem<BN, STAGES, CL, LN>;
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_2d_bf16(&ta, g.a, g.k, g.m, static_cast<uint64_t>(g.k) * 2, BK, BM, true) ||
-      !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, BN / CL, true) ||
+      !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, CL > 1 ? BN / 2 : BN, true) ||
       !make_tmap_2d_bf16(&tc, g.c, g.n, g.m, static_cast<uint64_t>(g.n) * 2, BK, kEpiRows, true))
     return cudaErrorInvalidValue;
   if (RESIDUAL) {
@@ -331,7 +475,7 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   } else {
     tr = tc;  // unused
   }
-  auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL>;
+  auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL, LN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kAlloc);
@@ -339,11 +483,29 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
     attr_set = true;
   }
   const int m_blocks = (g.m + BM - 1) / BM, n_blocks = (g.n + BN - 1) / BN;
-  const int units = ((m_blocks + CL - 1) / CL) * n_blocks;
-  const int max_units = device_sm_count() / CL;
-  const int grid = (units < max_units ? units : max_units) * CL;
+  const int units = ((m_blocks + (CL > 1 ? 1 : 0)) / (CL > 1 ? 2 : 1)) * (LN ? 1 : n_blocks);
+  // persistent grid = the clusters that can be co-resident (clusters of 4 cannot use every SM: GPC
+  // boundaries strand some), so no cluster waits for a second wave
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * (device_sm_count() / CL));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = S::kAlloc;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = device_sm_count() / CL;
+    max_clusters = n;
+  }
+  const int grid = (units < max_clusters ? units : max_clusters) * CL;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), S::kAlloc, stream, CL, ta, tb, tc, tr,
-                    static_cast<const __nv_bfloat16*>(g.bias), g.m, g.n, g.k, g.act);
+                    static_cast<const __nv_bfloat16*>(g.bias), g.ln_gamma, g.ln_beta, g.ln_eps, g.m, g.n, g.k, g.act);
 }
 
 }  // namespace
@@ -355,6 +517,17 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   if (g.residual != nullptr)
     return pair ? run_gemm<256, 5, true, 2>(g, stream) : run_gemm<256, 3, true, 1>(g, stream);
   return pair ? run_gemm<256, 5, false, 2>(g, stream) : run_gemm<256, 3, false, 1>(g, stream);
+}
+
+bool gemm_ln_supported(const GemmArgs& g) {
+  return g.n == 512 && g.residual != nullptr && g.ln_gamma != nullptr && g.ln_beta != nullptr &&
+         ((g.m + BM - 1) / BM) >= 2;
+}
+
+cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream) {
+  if (g.m == 0) return cudaSuccess;
+  if (!gemm_ln_supported(g)) return cudaErrorInvalidValue;
+  return run_gemm<256, 4, true, 4, true>(g, stream);  // 2 CTA pairs per cluster, 4 stages (LN smem)
 }
 
 }  // namespace cora

@@ -157,6 +157,31 @@ def test_linear_epilogues(act, use_res, m, n, k):
     assert rel_err(to_np(c), ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("m,k", [(300, 512), (4099, 512), (257, 2048), (1000, 2048)])
+@pytest.mark.parametrize("use_bias", [True, False])
+def test_linear_residual_layernorm_fused(m, k, use_bias):
+    n = 512
+    a = synth.round_bf16(synth.normal((m, k), 41))
+    w = synth.round_bf16(synth.normal((n, k), 42) / math.sqrt(k))
+    b = synth.round_bf16(synth.normal((n,), 43)) if use_bias else None
+    r = synth.round_bf16(synth.normal((m, n), 44))
+    g = synth.round_f32(1 + 0.1 * synth.normal((n,), 45))
+    be = synth.round_f32(0.1 * synth.normal((n,), 46))
+    c = P().linear_residual_layernorm(bf16_cuda(a), bf16_cuda(w), bf16_cuda(r), f32_cuda(g), f32_cuda(be),
+                                      bias=bf16_cuda(b) if use_bias else None)
+    ref = oracle.layernorm(oracle.linear(a, w, b, residual=r), g, be)
+    assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
+def test_linear_residual_layernorm_unsupported_shape():
+    a = bf16_cuda(synth.normal((300, 64), 1))
+    w = bf16_cuda(synth.normal((256, 64), 2))
+    r = bf16_cuda(synth.normal((300, 256), 3))
+    g = f32_cuda(np.ones(256))
+    with pytest.raises(Exception):
+        P().linear_residual_layernorm(a, w, r, g, g)
+
+
 # ---------------------------------------------------------------- a3: fused ragged attention
 ATTN_CASES = [
     [3, 7, 1, 5],
