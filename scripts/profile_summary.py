@@ -40,7 +40,10 @@ def read_csv_after_header(path, first_col):
 
 
 def launches(tag_dir):
-    rows = read_csv_after_header(os.path.join(tag_dir, "launches.csv"), "ID")
+    path = os.path.join(tag_dir, "launches.csv")
+    if not os.path.exists(path):
+        return None
+    rows = read_csv_after_header(path, "ID")
     if not rows:
         return None
     hdr = rows[0]
