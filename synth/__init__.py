@@ -154,4 +154,24 @@ def config(name: str):
         return dataset_lengths("wiki512", 128), 512, 8, 2048
     if name == "C4-race":
         return dataset_lengths("race", 128), 512, 8, 2048
+    # C5 padding-sensitivity sweep (BASELINE.json configs[4]): bs 32/64/128 x {all 512, U[1,512], skewed}
+    if name.startswith("C5-"):
+        _, kind, bs = name.split("-")
+        B = int(bs)
+        if kind == "equal":
+            return np.full(B, 512, dtype=np.int64), 512, 8, 2048
+        if kind == "uniform":
+            return uniform_lengths(B, 1, 512, seed=2000 + B), 512, 8, 2048
+        if kind == "skewed":
+            return skewed_lengths(B, 512, seed=3000 + B), 512, 8, 2048
+    # the other Table-3 datasets at bs 32/64/128: "<dataset>-<bs>"
+    if "-" in name and name.split("-")[0] in DATASETS:
+        ds, bs = name.split("-")
+        return dataset_lengths(ds, int(bs)), 512, 8, 2048
     raise KeyError(name)
+
+
+SWEEP_CONFIGS = ["C2-mnli", "C2-mrpc", "C3", "C4-wiki512", "C4-race"] + [
+    f"C5-{k}-{b}" for k in ("equal", "uniform", "skewed") for b in (32, 64, 128)]
+# the 24 cells of the paper's encoder-layer table (Table 4), synthetic lengths
+TABLE4_CONFIGS = [f"{ds}-{b}" for ds in DATASETS for b in (32, 64, 128)]
