@@ -53,5 +53,5 @@ from .encoder import (  # noqa: F401
     relu,
     gelu_erf,
 )
-from .flops import useful_flops, padded_flops, useful_macs_bruteforce, padded_macs_bruteforce, qkt_macs  # noqa: F401
+from .flops import useful_flops, padded_flops, useful_macs_bruteforce, padded_macs_bruteforce, qkt_macs, causal_attention_flops  # noqa: F401
 from .shard import shard_cost, shard_plan  # noqa: F401

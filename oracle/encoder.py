@@ -118,11 +118,14 @@ def ragged_softmax(x_flat: np.ndarray, lengths: Sequence[int], heads: int) -> np
     return out
 
 
-def ragged_attention(qkv: np.ndarray, lengths: Sequence[int], heads: int) -> np.ndarray:
+def ragged_attention(qkv: np.ndarray, lengths: Sequence[int], heads: int, causal: bool = False) -> np.ndarray:
     """O[T, d] = concat_h softmax(Q_h K_h^T / sqrt(d_h)) V_h per sequence.
 
     PAPER.md:296-300 (SDPA sub-module), 2256-2259 (QK^T, Softmax, AttnV);
     only j < L_b exist (no padded keys, no mask within a sequence: encoder).
+    causal=True: the masked MHA of the decoder (App. D.3
+    1752-1806): "the upper half of the attention matrix is masked", i.e. query
+    i attends to keys j <= i of its own sequence only (lower-triangular S).
     """
     T, three_d = qkv.shape
     d = three_d // 3
@@ -138,7 +141,10 @@ def ragged_attention(qkv: np.ndarray, lengths: Sequence[int], heads: int) -> np.
             q = qkv[r0:r0 + L, h * dh:(h + 1) * dh]
             k = qkv[r0:r0 + L, d + h * dh:d + (h + 1) * dh]
             v = qkv[r0:r0 + L, 2 * d + h * dh:2 * d + (h + 1) * dh]
-            p = softmax_row((q @ k.T) * (1.0 / math.sqrt(dh)))
+            sc = (q @ k.T) * (1.0 / math.sqrt(dh))
+            if causal:
+                sc = np.where(np.tril(np.ones((L, L), dtype=bool)), sc, -np.inf)
+            p = softmax_row(sc)
             out[r0:r0 + L, h * dh:(h + 1) * dh] = p @ v
     return out
 

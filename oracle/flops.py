@@ -60,3 +60,9 @@ def qkt_macs(lengths: Sequence[int], heads: int, head_dim: int, pad_to: Optional
     if pad_to is not None:
         lengths = [int(pad_to)] * len(lengths)
     return heads * head_dim * sum(int(L) * int(L) for L in lengths)
+
+
+def causal_attention_flops(lengths: Sequence[int], d: int) -> int:
+    """Useful FLOPs of masked (causal) SDPA: QK^T and AttnV over the lower triangle incl. the diagonal,
+    4 d * sum L (L + 1) / 2 ("a batch of lower triangular matrices")."""
+    return 4 * d * sum(int(L) * (int(L) + 1) // 2 for L in lengths)

@@ -195,3 +195,33 @@ def test_encoder_layer_zero_length_sequences():
     got = oracle.encoder_layer(x, lengths, w)
     alone = np.concatenate([oracle.encoder_layer(x[:3], [3], w), oracle.encoder_layer(x[3:], [2], w)])
     assert np.array_equal(got, alone)
+
+
+def test_causal_attention_b1_is_textbook_causal_sdpa():
+    L, H, d = 29, 2, 16
+    qkv = _qkv([L], d, seed=9)
+    got = oracle.ragged_attention(qkv, [L], H, causal=True)
+    q, k, v = (_t(qkv[:, i * d:(i + 1) * d]).reshape(L, H, d // H).transpose(0, 1) for i in range(3))
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(0, 1).reshape(L, d).numpy()
+    assert np.abs(got - ref).max() < 1e-13
+
+
+def test_causal_attention_invariants():
+    lengths, H, d = [5, 1, 7], 2, 16
+    qkv = _qkv(lengths, d, seed=10)
+    out = oracle.ragged_attention(qkv, lengths, H, causal=True)
+    ro = oracle.row_offsets(lengths)
+    # the first query of every sequence sees only its own key: O = V exactly
+    for b in range(len(lengths)):
+        assert np.array_equal(out[ro[b]], qkv[ro[b], 2 * d:])
+    # the last query of a sequence sees every key: identical to the unmasked row
+    full = oracle.ragged_attention(qkv, lengths, H)
+    for b, L in enumerate(lengths):
+        assert np.abs(out[ro[b] + L - 1] - full[ro[b] + L - 1]).max() < 1e-14
+    # row i does not depend on later keys of its sequence
+    qkv2 = qkv.copy()
+    qkv2[ro[2] + 4:ro[2] + 7, d:] += 5.0
+    out2 = oracle.ragged_attention(qkv2, lengths, H, causal=True)
+    assert np.array_equal(out[:ro[2] + 4], out2[:ro[2] + 4])
+    # FLOP count of the lower triangle
+    assert oracle.causal_attention_flops([3], 8) == 4 * 8 * 6
