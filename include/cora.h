@@ -207,6 +207,12 @@ cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, c
 cora_status_t cora_ragged_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o, int32_t head_dim,
                                         float scale, void* stream);
 
+/* Masked (causal) variant: query i of sequence b attends to keys j <= i of b only -- the decoder's
+ * masked MHA as a batch of lower-triangular ragged matrices (App. D.3
+ * PAPER.md:1752-1806).  KV tiles above the diagonal are neither loaded nor computed. */
+cora_status_t cora_ragged_masked_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o,
+                                               int32_t head_dim, float scale, void* stream);
+
 /* Row softmax of the ragged attention matrix X[b, i, h, 0:L_b] stored flat at offset
  * H*attn_off[b] + (i*H + h)*L_b (App. B.1 lowering); x and y have
  * H * sum_b L_b^2 elements of dtype dt.  Warp-wide reductions. */

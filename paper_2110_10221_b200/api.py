@@ -228,7 +228,7 @@ def linear_residual_layernorm(a: torch.Tensor, w: torch.Tensor, residual: torch.
 
 
 def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, scale: Optional[float] = None,
-                     out=None, stream=None) -> torch.Tensor:
+                     out=None, stream=None, causal: bool = False) -> torch.Tensor:
     _need_cuda(qkv)
     T = layout.total_tokens
     d = layout.heads * head_dim
@@ -236,8 +236,9 @@ def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, sca
         raise ValueError("qkv must be bf16 [T, 3 * heads * head_dim]")
     o = torch.empty(T, d, dtype=torch.bfloat16, device=qkv.device) if out is None else out
     s = head_dim ** -0.5 if scale is None else scale
-    C.check(C.lib().cora_ragged_attention_fwd(ctypes.byref(layout.c), _ptr(qkv), _ptr(o), head_dim, s,
-                                              _stream(stream)), "cora_ragged_attention_fwd")
+    fn = C.lib().cora_ragged_masked_attention_fwd if causal else C.lib().cora_ragged_attention_fwd
+    C.check(fn(ctypes.byref(layout.c), _ptr(qkv), _ptr(o), head_dim, s, _stream(stream)),
+            "cora_ragged_masked_attention_fwd" if causal else "cora_ragged_attention_fwd")
     return o
 
 

@@ -247,6 +247,15 @@ cora_status_t cora_ragged_attention_fwd(const cora_layout_t* layout, const void*
   return cuda_status(launch_attention(*layout, qkv, o, head_dim, scale, as_stream(stream)));
 }
 
+cora_status_t cora_ragged_masked_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o,
+                                               int32_t head_dim, float scale, void* stream) {
+  if (layout == nullptr || head_dim <= 0 || head_dim > 128 || (head_dim % 2) != 0) return CORA_ERR_INVALID;
+  if (layout->total_tokens == 0 || layout->batch == 0) return CORA_OK;
+  if (qkv == nullptr || o == nullptr || !aligned16(qkv) || !aligned16(o)) return CORA_ERR_INVALID;
+  if (((layout->heads * head_dim) % 8) != 0) return CORA_ERR_INVALID;
+  return cuda_status(launch_attention(*layout, qkv, o, head_dim, scale, as_stream(stream), /*causal=*/true));
+}
+
 cora_status_t cora_ragged_softmax_fwd(const cora_layout_t* layout, const void* x, void* y, cora_dtype_t dt,
                                       void* stream) {
   if (layout == nullptr || (dt != CORA_DT_BF16 && dt != CORA_DT_F32)) return CORA_ERR_INVALID;

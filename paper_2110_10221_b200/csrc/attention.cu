@@ -75,6 +75,27 @@ __device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* 
   return WorkTile{(w >> 16) & 0xFF, (w >> 24) & 0x7F, sq.x, sq.y};
 }
 
+// The walk of one CTA: bidirectional attention visits single q-tiles of the longest-first tile list;
+// causal attention visits the UNIT list (same longest-first order, ceil(nq/2) units per (b, h)) and
+// processes unit qp as the q-tile pair (nq-1-qp, qp), whose KV work (nq-qp) + (qp+1) = nq+1 is the
+// same for every unit of a sequence (a lone middle tile when nq is odd), so the static stride over a
+// work-sorted list stays balanced although causal q-tiles have 1..nq KV tiles.
+struct WorkUnit {
+  int h, r0, L, qt0, qt1, count;
+  __device__ __forceinline__ WorkTile tile(int sub) const { return WorkTile{h, sub ? qt1 : qt0, r0, L}; }
+};
+template <bool CAUSAL>
+__device__ __forceinline__ WorkUnit load_work(const int32_t* list, const int2* list_seq, int idx) {
+  const WorkTile t = load_tile(list, list_seq, idx);
+  if (!CAUSAL) return WorkUnit{t.h, t.r0, t.L, t.qt, t.qt, 1};
+  const int nq = (t.L + TQ - 1) / TQ, qp = t.qt;
+  return WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2};
+}
+
+// CAUSAL: masked MHA (App. D.3): query i attends to keys j <= i of its sequence, so
+// q-tile qt needs only KV tiles j <= qt (the "lower triangular" ragged loop -- tiles above the diagonal
+// are never loaded or computed) and the diagonal tile is masked per element.
+template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
                          const int2* __restrict__ tile_seq, const int32_t* __restrict__ n_tiles_ptr,
@@ -137,32 +158,38 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t q_ph = 0, k_ph = 0;
       int qs = 0, ks = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkTile cur = load_tile(tiles, tile_seq, idx);
-        const int nkv = (cur.L + TK - 1) / TK;
-        mbar_wait<false>(&q_empty[qs], q_ph ^ 1);
-        mbar_arrive_expect_tx(&q_full[qs], kTileBytes);
-        tma_load_2d(smem + AttnSmem::kOffQ + qs * kTileBytes, &tm_qkv, &q_full[qs], cur.h * HD, cur.r0 + cur.qt * TQ);
-        if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
-        for (int j = 0; j < nkv; ++j) {
-          mbar_wait<false>(&k_empty[ks], k_ph ^ 1);
-          mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
-          tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
-                      cur.r0 + j * TK);
-          if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+        const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
+          mbar_wait<false>(&q_empty[qs], q_ph ^ 1);
+          mbar_arrive_expect_tx(&q_full[qs], kTileBytes);
+          tma_load_2d(smem + AttnSmem::kOffQ + qs * kTileBytes, &tm_qkv, &q_full[qs], cur.h * HD, cur.r0 + cur.qt * TQ);
+          if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
+          for (int j = 0; j < nkv; ++j) {
+            mbar_wait<false>(&k_empty[ks], k_ph ^ 1);
+            mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
+            tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
+                        cur.r0 + j * TK);
+            if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+          }
         }
       }
     } else if (lane == 1) {
       uint32_t v_ph = 0;
       int vs = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkTile cur = load_tile(tiles, tile_seq, idx);
-        const int nkv = (cur.L + TK - 1) / TK;
-        for (int j = 0; j < nkv; ++j) {
-          mbar_wait<false>(&v_empty[vs], v_ph ^ 1);
-          mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
-          tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
-                      cur.r0 + j * TK);
-          if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
+        const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
+          for (int j = 0; j < nkv; ++j) {
+            mbar_wait<false>(&v_empty[vs], v_ph ^ 1);
+            mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
+            tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
+                        cur.r0 + j * TK);
+            if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
+          }
         }
       }
     }
@@ -174,48 +201,51 @@ __global__ void __launch_bounds__(kThreads, 2)
       int qs = 0, ks = 0, vs = 0;
       uint32_t q_ph = 0, k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkTile cur = load_tile(tiles, tile_seq, idx);
-        const int nkv = (cur.L + TK - 1) / TK;
-        mbar_wait<false>(&q_full[qs], q_ph);
-        const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
-        auto issue_s = [&](bool last) {
-          mbar_wait<false>(&k_full[ks], k_ph);
-          mbar_wait<false>(s_empty, s_ph ^ 1);
-          s_ph ^= 1;
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
-#pragma unroll
-          for (int k = 0; k < HD / 16; ++k)
-            umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
-                         make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
-          umma_commit(&k_empty[ks]);
-          umma_commit(s_full);
-          if (last) umma_commit(&q_empty[qs]);  // Q slot free once the last S of the tile is done
-          if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-        };
-        issue_s(nkv == 1);
-        for (int j = 0; j < nkv; ++j) {
-          if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
-          mbar_wait<false>(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
-          p_ph ^= 1;
-          mbar_wait<false>(&v_full[vs], v_ph);
-          if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
-            mbar_wait<false>(o_empty, o_ph ^ 1);
-            o_ph ^= 1;
+        const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
+          mbar_wait<false>(&q_full[qs], q_ph);
+          const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
+          auto issue_s = [&](bool last) {
+            mbar_wait<false>(&k_full[ks], k_ph);
+            mbar_wait<false>(s_empty, s_ph ^ 1);
+            s_ph ^= 1;
+            tc_fence_after();
+            const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
+  #pragma unroll
+            for (int k = 0; k < HD / 16; ++k)
+              umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
+                           make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
+            umma_commit(&k_empty[ks]);
+            umma_commit(s_full);
+            if (last) umma_commit(&q_empty[qs]);  // Q slot free once the last S of the tile is done
+            if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+          };
+          issue_s(nkv == 1);
+          for (int j = 0; j < nkv; ++j) {
+            if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
+            mbar_wait<false>(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
+            p_ph ^= 1;
+            mbar_wait<false>(&v_full[vs], v_ph);
+            if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
+              mbar_wait<false>(o_empty, o_ph ^ 1);
+              o_ph ^= 1;
+            }
+            tc_fence_after();
+            const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV + vs * kTileBytes);
+  #pragma unroll
+            for (int k = 0; k < TK / 16; ++k) {
+              // A = P from TMEM (16 keys = 8 packed columns per step), B = V (MN-major, 16 key rows per step)
+              const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
+              umma_bf16_ts(tmem_base + kTmemO, tmem_base + kTmemP + k * 8, vd, idesc_o, (j | k) != 0);
+            }
+            umma_commit(&v_empty[vs]);
+            umma_commit(pv_done);
+            if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
           }
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV + vs * kTileBytes);
-#pragma unroll
-          for (int k = 0; k < TK / 16; ++k) {
-            // A = P from TMEM (16 keys = 8 packed columns per step), B = V (MN-major, 16 key rows per step)
-            const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
-            umma_bf16_ts(tmem_base + kTmemO, tmem_base + kTmemP + k * 8, vd, idesc_o, (j | k) != 0);
-          }
-          umma_commit(&v_empty[vs]);
-          umma_commit(pv_done);
-          if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
+          if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
         }
-        if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
       }
     }
   } else {
@@ -225,126 +255,134 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t t_lane = (qd * 32) << 16;
     uint32_t s_ph = 0, pv_ph = 0;
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-      const WorkTile cur = load_tile(tiles, tile_seq, idx);
-      const int L = cur.L;
-      const int nkv = (L + TK - 1) / TK;
-      if (cur.qt * TQ + static_cast<int>(qd) * 32 >= L) {
-        // none of this warp's 32 query rows belongs to the sequence: keep the barrier protocol,
-        // skip the math (its P rows are stale, its O rows are never stored)
-        for (int j = 0; j < nkv; ++j) {
-          mbar_wait<false>(s_full, s_ph);
-          s_ph ^= 1;
-          tc_fence_after();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_empty);
-          if (j > 0) {
-            mbar_wait<false>(pv_done, pv_ph);
-            pv_ph ^= 1;
+      const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+      for (int sub = 0; sub < wu.count; ++sub) {
+        const WorkTile cur = wu.tile(sub);
+        const int L = cur.L;
+        const int nkv = CAUSAL ? min((L + TK - 1) / TK, cur.qt + 1) : (L + TK - 1) / TK;
+        if (cur.qt * TQ + static_cast<int>(qd) * 32 >= L) {
+          // none of this warp's 32 query rows belongs to the sequence: keep the barrier protocol,
+          // skip the math (its P rows are stale, its O rows are never stored)
+          for (int j = 0; j < nkv; ++j) {
+            mbar_wait<false>(s_full, s_ph);
+            s_ph ^= 1;
+            tc_fence_after();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_empty);
+            if (j > 0) {
+              mbar_wait<false>(pv_done, pv_ph);
+              pv_ph ^= 1;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(p_full);
-        }
-        mbar_wait<false>(pv_done, pv_ph);
-        pv_ph ^= 1;
-        tc_fence_after();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(o_empty);
-        continue;
-      }
-      float m_ref = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkv; ++j) {
-        const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
-        mbar_wait<false>(s_full, s_ph);
-        s_ph ^= 1;
-        tc_fence_after();
-        uint32_t sr[TK];
-#pragma unroll
-        for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
-        tmem_ld_wait();
-        // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty);
-        float* sv = reinterpret_cast<float*>(sr);
-        // row max over the valid keys (keys >= L_b masked to -inf in the tail tile)
-        if (valid < TK) {
-#pragma unroll
-          for (int c = 0; c < TK; ++c)
-            if (c >= valid) sv[c] = -INFINITY;
-        }
-        float m8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
-        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
-        // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
-        const bool bump = mx > m_ref + kRescaleLog2;
-        const float m_new = bump ? mx : m_ref;
-        const float alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
-        m_ref = m_new;
-        // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0), fp32 row sum in 8 chains,
-        // bf16 pairs packed right away (the A operand layout of the TS MMA: 2 keys per column)
-        float r8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) r8[k] = 0.f;
-        uint32_t pk[TK / 2];
-#pragma unroll
-        for (int c = 0; c < TK; c += 2) {
-          const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
-          const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
-          r8[(c >> 1) & 7] += p0 + p1;
-          pk[c / 2] = pack_bf16x2(p0, p1);
-        }
-        l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
-        if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
           mbar_wait<false>(pv_done, pv_ph);
           pv_ph ^= 1;
           tc_fence_after();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(o_empty);
+          continue;
         }
-        CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP, pk);
-        CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP + 32, (pk + 32));
-        // rescale the O accumulator in place when some row of this warp moved its reference max
-        if (j > 0 && __any_sync(0xffffffffu, bump)) {
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            uint32_t orr[32];
-            const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
-            CORA_TMEM_LD_32X32B_X32(taddr, orr);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-            CORA_TMEM_ST_32X32B_X32(taddr, orr);
+        float m_ref = -INFINITY, l = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+          const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
+          mbar_wait<false>(s_full, s_ph);
+          s_ph ^= 1;
+          tc_fence_after();
+          uint32_t sr[TK];
+  #pragma unroll
+          for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
+          tmem_ld_wait();
+          // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty);
+          float* sv = reinterpret_cast<float*>(sr);
+          // row max over the valid keys (keys >= L_b masked to -inf in the tail tile; with CAUSAL also the
+          // keys after the query in the diagonal tile)
+          if (CAUSAL && j == cur.qt) {
+  #pragma unroll
+            for (int c = 0; c < TK; ++c)
+              if (c > i || c >= valid) sv[c] = -INFINITY;
+          } else if (valid < TK) {
+  #pragma unroll
+            for (int c = 0; c < TK; ++c)
+              if (c >= valid) sv[c] = -INFINITY;
           }
+          float m8[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+  #pragma unroll
+          for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
+          // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
+          const bool bump = mx > m_ref + kRescaleLog2;
+          const float m_new = bump ? mx : m_ref;
+          const float alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
+          m_ref = m_new;
+          // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0), fp32 row sum in 8 chains,
+          // bf16 pairs packed right away (the A operand layout of the TS MMA: 2 keys per column)
+          float r8[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) r8[k] = 0.f;
+          uint32_t pk[TK / 2];
+  #pragma unroll
+          for (int c = 0; c < TK; c += 2) {
+            const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
+            const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
+            r8[(c >> 1) & 7] += p0 + p1;
+            pk[c / 2] = pack_bf16x2(p0, p1);
+          }
+          l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
+          if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
+            mbar_wait<false>(pv_done, pv_ph);
+            pv_ph ^= 1;
+            tc_fence_after();
+          }
+          CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP, pk);
+          CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP + 32, (pk + 32));
+          // rescale the O accumulator in place when some row of this warp moved its reference max
+          if (j > 0 && __any_sync(0xffffffffu, bump)) {
+  #pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint32_t orr[32];
+              const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
+              CORA_TMEM_LD_32X32B_X32(taddr, orr);
+              tmem_ld_wait();
+  #pragma unroll
+              for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+              CORA_TMEM_ST_32X32B_X32(taddr, orr);
+            }
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full);
         }
-        tmem_st_wait();
+        // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
+        mbar_wait<false>(pv_done, pv_ph);
+        pv_ph ^= 1;
+        tc_fence_after();
+        uint32_t orr[HD];
+        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
+        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
+        tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
-      }
-      // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
-      mbar_wait<false>(pv_done, pv_ph);
-      pv_ph ^= 1;
-      tc_fence_after();
-      uint32_t orr[HD];
-      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
-      CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_empty);
-      const int qrow = cur.qt * TQ + i;
-      if (qrow < L) {
-        const float inv = 1.f / l;
-        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD);
-#pragma unroll
-        for (int g = 0; g < HD / 8; ++g) {
-          const float* o = reinterpret_cast<const float*>(orr) + g * 8;
-          dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
-                              pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+        if (lane == 0) mbar_arrive(o_empty);
+        const int qrow = cur.qt * TQ + i;
+        if (qrow < L) {
+          const float inv = 1.f / l;
+          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD);
+  #pragma unroll
+          for (int g = 0; g < HD / 8; ++g) {
+            const float* o = reinterpret_cast<const float*>(orr) + g * 8;
+            dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
+                                pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+          }
         }
       }
     }
@@ -366,14 +404,15 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(const __nv_bfloat16
                                                              const int32_t* __restrict__ lengths,
                                                              const int32_t* __restrict__ row_off,
                                                              const int32_t* __restrict__ seq_of_tok, int32_t T,
-                                                             int32_t heads, int32_t hd, float scale) {
+                                                             int32_t heads, int32_t hd, float scale, int causal) {
   const int lane = threadIdx.x & 31;
   const int64_t wg = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wg >= static_cast<int64_t>(T) * heads) return;
   const int t = static_cast<int>(wg / heads), h = static_cast<int>(wg % heads);
   const int b = seq_of_tok[t];
   if (b < 0) return;
-  const int L = lengths[b], r0 = row_off[b];
+  const int r0 = row_off[b];
+  const int L = causal ? (t - r0 + 1) : lengths[b];  // keys j < L of the sequence (j <= i when causal)
   const int d = heads * hd, ld = 3 * d;
   const __nv_bfloat16* q = qkv + static_cast<size_t>(t) * ld + h * hd;
   float m = -INFINITY, l = 0.f, o[DPL];
@@ -423,7 +462,7 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(const __nv_bfloat16
 }  // namespace
 
 cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, bool causal) {
   if (L.total_tokens == 0 || L.batch == 0) return cudaSuccess;
   const int32_t d = L.heads * head_dim;
   if (head_dim == HD) {
@@ -432,18 +471,25 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
       return cudaErrorInvalidValue;
     static bool attr_set = false;
     if (!attr_set) {
-      cudaError_t e =
-          cudaFuncSetAttribute(attention_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem::kAlloc);
-      if (e != cudaSuccess) return e;
+      for (auto k : {attention_fwd_kernel<false>, attention_fwd_kernel<true>}) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem::kAlloc);
+        if (e != cudaSuccess) return e;
+      }
       attr_set = true;
     }
     const int max_grid = 2 * device_sm_count();
     const int grid = L.n_tiles_max < max_grid ? L.n_tiles_max : max_grid;
     if (grid == 0) return cudaSuccess;
     const float scale_log2 = scale * 1.4426950408889634f;
-    return launch_pdl(attention_fwd_kernel, dim3(grid), dim3(kThreads), AttnSmem::kAlloc, stream, 1, tm, L.tiles,
-                      reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, static_cast<__nv_bfloat16*>(o), d,
-                      scale_log2);
+    if (causal) {
+      const int ugrid = L.n_units_max < max_grid ? L.n_units_max : max_grid;
+      return launch_pdl(attention_fwd_kernel<true>, dim3(ugrid > 0 ? ugrid : 1), dim3(kThreads), AttnSmem::kAlloc,
+                        stream, 1, tm, L.units, reinterpret_cast<const int2*>(L.unit_seq), L.n_units,
+                        static_cast<__nv_bfloat16*>(o), d, scale_log2);
+    }
+    return launch_pdl(attention_fwd_kernel<false>, dim3(grid), dim3(kThreads), AttnSmem::kAlloc, stream, 1, tm,
+                      L.tiles, reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, static_cast<__nv_bfloat16*>(o),
+                      d, scale_log2);
   }
   const int64_t warps = static_cast<int64_t>(L.total_tokens) * L.heads;
   const dim3 block(256), grid(static_cast<unsigned>((warps + 7) / 8));
@@ -451,10 +497,10 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
   auto out = static_cast<__nv_bfloat16*>(o);
   if (head_dim <= 32)
     attention_simt_kernel<1><<<grid, block, 0, stream>>>(q, out, L.lengths, L.row_off, L.seq_of_tok,
-                                                         L.total_tokens, L.heads, head_dim, scale);
+                                                         L.total_tokens, L.heads, head_dim, scale, causal ? 1 : 0);
   else
     attention_simt_kernel<4><<<grid, block, 0, stream>>>(q, out, L.lengths, L.row_off, L.seq_of_tok,
-                                                         L.total_tokens, L.heads, head_dim, scale);
+                                                         L.total_tokens, L.heads, head_dim, scale, causal ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -33,7 +33,7 @@ bool gemm_ln_supported(const GemmArgs& g);
 cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream);
 
 cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
-                             cudaStream_t stream);
+                             cudaStream_t stream, bool causal = false);
 
 cudaError_t launch_layernorm(const void* x, const void* residual, const float* gamma, const float* beta, void* y,
                              int32_t rows, int32_t cols, float eps, cora_dtype_t dt, cudaStream_t stream);

@@ -1,7 +1,7 @@
-"""Time the fused attention kernel alone on a BASELINE config (profiling helper).
+"""Time the fused attention kernel alone (bidirectional and causal) on BASELINE configs (profiling helper).
 
-    python scripts/time_attention.py [config] [reps]
-Env CORA_ATTN_MODE selects the profiling variants of attention_fwd_kernel (see attention.cu).
+    python scripts/time_attention.py [config[,config...]] [reps]
+Useful FLOPs: 4 d sum L^2 (bidirectional), 4 d sum L(L+1)/2 (causal).
 """
 import os
 import sys
@@ -15,22 +15,37 @@ import torch
 import synth
 import paper_2110_10221_b200 as P
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "C4-wiki512"
+cfgs = (sys.argv[1] if len(sys.argv) > 1 else "C4-wiki512").split(",")
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
-lengths, d, H, dff = synth.config(cfg)
-T = int(lengths.sum())
-qkv = torch.randn(T, 3 * d, device="cuda").to(torch.bfloat16)
-lay = P.layout_build(torch.tensor(lengths, dtype=torch.int32, device="cuda"), T, H, 512)
-o = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
-for _ in range(5):
-    P.ragged_attention(lay, qkv, 64, out=o)
-torch.cuda.synchronize()
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-ev[0].record()
-for _ in range(reps):
-    P.ragged_attention(lay, qkv, 64, out=o)
-ev[1].record()
-torch.cuda.synchronize()
-us = ev[0].elapsed_time(ev[1]) / reps * 1e3
-S2 = int((lengths.astype(np.int64) ** 2).sum())
-print(f"{cfg} mode={os.environ.get('CORA_ATTN_MODE', '0')} attention {us:.1f} us  {4 * d * S2 / us / 1e6:.1f} TFLOP/s")
+
+
+def time_us(fn):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(reps):
+        fn()
+    ev[1].record()
+    torch.cuda.synchronize()
+    return ev[0].elapsed_time(ev[1]) / reps * 1e3
+
+
+for cfg in cfgs:
+    if cfg.startswith("L"):  # "L<len>x<batch>": equal lengths
+        ln, bs = cfg[1:].split("x")
+        lengths, d, H = np.full(int(bs), int(ln), dtype=np.int64), 512, 8
+    else:
+        lengths, d, H, _ = synth.config(cfg)
+    T = int(lengths.sum())
+    qkv = torch.randn(T, 3 * d, device="cuda").to(torch.bfloat16)
+    lay = P.layout_build(torch.tensor(lengths, dtype=torch.int32, device="cuda"), T, H, 512)
+    o = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    L = lengths.astype(np.int64)
+    full = time_us(lambda: P.ragged_attention(lay, qkv, 64, out=o))
+    causal = time_us(lambda: P.ragged_attention(lay, qkv, 64, out=o, causal=True))
+    f_full = 4 * d * int((L * L).sum())
+    f_causal = 4 * d * int((L * (L + 1) // 2).sum())
+    print(f"{cfg}: attention {full:.1f} us {f_full / full / 1e6:.1f} TFLOP/s | causal {causal:.1f} us "
+          f"{f_causal / causal / 1e6:.1f} TFLOP/s | ratio {full / causal:.2f}x", flush=True)

@@ -204,6 +204,16 @@ def test_ragged_attention(lengths, head_dim, heads):
     assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, heads)) <= TOL_BF16
 
 
+@pytest.mark.parametrize("lengths", ATTN_CASES, ids=lambda l: f"B{len(l)}-T{sum(l)}")
+@pytest.mark.parametrize("head_dim,heads", [(64, 8), (8, 2)])
+def test_ragged_masked_attention(lengths, head_dim, heads):
+    d = heads * head_dim
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 33))
+    lay = _layout(lengths, heads)
+    o = P().ragged_attention(lay, bf16_cuda(qkv), head_dim, causal=True)
+    assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, heads, causal=True)) <= TOL_BF16
+
+
 def test_attention_poisoned_output_untouched_rows_none():
     # every output row belongs to some sequence: all are written; NaN-poison must disappear
     lengths = [5, 0, 129, 64]
