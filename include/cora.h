@@ -158,6 +158,11 @@ size_t cora_encoder_workspace_bytes(const cora_encoder_params_t* p, int32_t tota
 cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
                                      void* y, void* ws, size_t ws_bytes, void* stream);
 
+/* Kernel launches cora_encoder_layer_fwd makes for this configuration (prelude excluded): 5 when the
+ * two "GEMM + bias + residual, LayerNorm" pairs are fused (d_model == 512, total_tokens > 128 and
+ * non-NULL LayerNorm parameters), else 7; 0 when total_tokens == 0; -1 on a NULL p or negative T. */
+int32_t cora_encoder_layer_launches(const cora_encoder_params_t* p, int32_t total_tokens);
+
 /* Number of events cora_encoder_layer_fwd_ex records (one before each of the 7 kernels + one after). */
 #define CORA_LAYER_EVENTS 8
 

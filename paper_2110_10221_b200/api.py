@@ -146,6 +146,10 @@ class EncoderLayer:
     def workspace_bytes(self, total_tokens: int) -> int:
         return C.lib().cora_encoder_workspace_bytes(ctypes.byref(self.cp), int(total_tokens))
 
+    def launches(self, total_tokens: int) -> int:
+        """Kernels one layer call launches (5 with the fused GEMM + LayerNorm epilogues, else 7)."""
+        return int(C.lib().cora_encoder_layer_launches(ctypes.byref(self.cp), int(total_tokens)))
+
     def __call__(self, x: torch.Tensor, layout: RaggedLayout, out: Optional[torch.Tensor] = None,
                  stream=None, events: Optional[Sequence["torch.cuda.Event"]] = None) -> torch.Tensor:
         """events: optional C.LAYER_EVENTS torch.cuda.Event objects recorded around every kernel."""

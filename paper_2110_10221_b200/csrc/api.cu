@@ -362,6 +362,15 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   return CORA_OK;
 }
 
+int32_t cora_encoder_layer_launches(const cora_encoder_params_t* p, int32_t total_tokens) {
+  if (p == nullptr || total_tokens < 0) return -1;
+  if (total_tokens == 0) return 0;
+  GemmArgs g{nullptr, p->w_o, p->b_o, p->w_o, nullptr, total_tokens, p->d_model, p->d_model, CORA_ACT_NONE};
+  g.ln_gamma = static_cast<const float*>(p->ln1_g);
+  g.ln_beta = static_cast<const float*>(p->ln1_b);
+  return gemm_ln_supported(g) ? 5 : 7;
+}
+
 cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
                                      void* y, void* ws, size_t ws_bytes, void* stream) {
   return cora_encoder_layer_fwd_ex(p, layout, x, y, ws, ws_bytes, stream, nullptr);

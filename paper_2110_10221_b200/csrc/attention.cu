@@ -49,6 +49,26 @@ constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
 // moved when a new score exceeds it by more than kRescaleLog2 (in log2 units), so P <= 2^8 and the
 // O accumulator in TMEM is rescaled rarely.  O / l is unchanged mathematically.
 constexpr float kRescaleLog2 = 8.0f;
+// MUFU offload (experiment, off): of every 4 consecutive key pairs, kPolyPairs are exponentiated on the
+// FMA pipe with a polynomial (exp2_poly) instead of MUFU.EX2.  Measured at C4: 0 -> 105 us, 1 -> 130 us,
+// 2 -> 174 us, 3 -> 225 us: the softmax warps are issue/latency-bound, not MUFU-bound (XU 45 %), so
+// the ~7 extra instructions per offloaded exponential cost more than the MUFU cycles they free.
+#ifndef CORA_ATTN_POLY_PAIRS
+#define CORA_ATTN_POLY_PAIRS 0
+#endif
+constexpr int kPolyPairs = CORA_ATTN_POLY_PAIRS;
+__device__ __forceinline__ constexpr bool poly_col(int c) { return ((c >> 1) & 3) < kPolyPairs; }
+
+// 2^x on the FMA/ALU pipes, x >= -125 (callers clamp or select): x = j + f with j = rint(x) by the
+// 1.5 * 2^23 magic-number add, f in [-1/2, 1/2]; 2^f by a degree-3 polynomial fitted for relative error
+// (max 2.1e-4, below the bf16 rounding of P, 3.9e-3); 2^j added into the exponent field.  The integer
+// part of t = x + 1.5 * 2^23 sits in its low mantissa bits, so (bits(t) << 23) == j << 23 (mod 2^32).
+__device__ __forceinline__ float exp2_poly(float x) {
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.053027520f, f, 0.24221394f), f, 0.69357257f), f, 0.99995904f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 struct AttnSmem {
   static constexpr int kOffQ = 0;
@@ -149,6 +169,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   pdl_wait();  // QKV (previous kernel) complete and visible
   pdl_trigger();
   const int n_tiles = *n_tiles_ptr;
+  // every role walks the same tiles; the next tile's metadata load is issued one tile ahead
+  WorkUnit wu_next{};
+  if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producers
@@ -158,7 +181,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t q_ph = 0, k_ph = 0;
       int qs = 0, ks = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+        const WorkUnit wu = wu_next;
+        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
         for (int sub = 0; sub < wu.count; ++sub) {
           const WorkTile cur = wu.tile(sub);
           const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
@@ -179,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       uint32_t v_ph = 0;
       int vs = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+        const WorkUnit wu = wu_next;
+        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
         for (int sub = 0; sub < wu.count; ++sub) {
           const WorkTile cur = wu.tile(sub);
           const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
@@ -201,7 +226,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       int qs = 0, ks = 0, vs = 0;
       uint32_t q_ph = 0, k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+        const WorkUnit wu = wu_next;
+        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
         for (int sub = 0; sub < wu.count; ++sub) {
           const WorkTile cur = wu.tile(sub);
           const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
@@ -255,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t t_lane = (qd * 32) << 16;
     uint32_t s_ph = 0, pv_ph = 0;
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-      const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);
+      const WorkUnit wu = wu_next;
+      if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
       for (int sub = 0; sub < wu.count; ++sub) {
         const WorkTile cur = wu.tile(sub);
         const int L = cur.L;
@@ -302,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           float* sv = reinterpret_cast<float*>(sr);
           // row max over the valid keys (keys >= L_b masked to -inf in the tail tile; with CAUSAL also the
           // keys after the query in the diagonal tile)
+          const bool masked = (CAUSAL && j == cur.qt) || valid < TK;
           if (CAUSAL && j == cur.qt) {
   #pragma unroll
             for (int c = 0; c < TK; ++c)
@@ -331,8 +359,16 @@ __global__ void __launch_bounds__(kThreads, 2)
           uint32_t pk[TK / 2];
   #pragma unroll
           for (int c = 0; c < TK; c += 2) {
-            const float p0 = ex2_approx(fmaf(sv[c], scale_log2, -m_ref));
-            const float p1 = ex2_approx(fmaf(sv[c + 1], scale_log2, -m_ref));
+            const float x0 = fmaf(sv[c], scale_log2, -m_ref), x1 = fmaf(sv[c + 1], scale_log2, -m_ref);
+            float p0, p1;
+            if (poly_col(c)) {
+              // masked keys (-inf) must give exactly 0 like EX2; unmasked x is clamped into the poly's range
+              p0 = masked ? (x0 > -125.f ? exp2_poly(x0) : 0.f) : exp2_poly(fmaxf(x0, -125.f));
+              p1 = masked ? (x1 > -125.f ? exp2_poly(x1) : 0.f) : exp2_poly(fmaxf(x1, -125.f));
+            } else {
+              p0 = ex2_approx(x0);
+              p1 = ex2_approx(x1);
+            }
             r8[(c >> 1) & 7] += p0 + p1;
             pk[c / 2] = pack_bf16x2(p0, p1);
           }

@@ -22,6 +22,8 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "cora_internal.h"
 #include "ptx.cuh"
@@ -502,6 +504,9 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = device_sm_count() / CL;
     max_clusters = n;
+    if (getenv("CORA_DEBUG") != nullptr)
+      fprintf(stderr, "cora gemm<BN=%d,ST=%d,RES=%d,CL=%d,LN=%d>: %d co-resident clusters, smem %d B\n", BN, STAGES,
+              int(RESIDUAL), CL, int(LN), n, S::kAlloc);
   }
   const int grid = (units < max_clusters ? units : max_clusters) * CL;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), S::kAlloc, stream, CL, ta, tb, tc, tr,

@@ -22,6 +22,8 @@ import sys
 STEP_ORDER = ["prelude", "qkv_gemm", "attention", "out_proj_gemm", "layernorm1", "ff1_gemm", "ff2_gemm",
               "layernorm2"]
 
+STEP_ORDER_FUSED = ["prelude", "qkv_gemm", "attention", "out_proj_gemm+ln1", "ff1_gemm", "ff2_gemm+ln2"]
+
 
 def short(name: str) -> str:
     for key in ("layout_merged", "layout_scan", "fusion_maps", "gemm", "attention_fwd", "attention_simt", "layernorm",
@@ -54,9 +56,12 @@ def launches(tag_dir):
     starts = [i for i, (k, _) in enumerate(ours) if k in ("layout_merged", "layout_scan")]
     if not starts:
         return None
-    last = ours[starts[-1]:starts[-1] + len(STEP_ORDER)]
+    last = ours[starts[-1]:]
+    # 5 layer kernels: LayerNorm fused into the out-proj / FF2 GEMM epilogues (d_model 512)
+    order = STEP_ORDER_FUSED if len(last) == len(STEP_ORDER_FUSED) else STEP_ORDER
+    last = last[:len(order)]
     named = []
-    for (k, t), want in zip(last, STEP_ORDER):
+    for (k, t), want in zip(last, order):
         named.append((want, k, t))
     return named
 
@@ -147,6 +152,9 @@ def main():
                 key = next(ln_keys)
             if key and d.get("dram_read") is not None:
                 traffic[key] = d["dram_read"] + (d.get("dram_write") or 0)
+        if "layernorm" not in order and order.count("gemm") == 4:
+            for k in ("layernorm1", "layernorm2"):  # fused into the GEMM epilogues: no kernel of their own
+                traffic.pop(k, None)
         traffic["_source"] = f"ncu --set full capture {tag_dir} (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         json.dump(traffic, open(tp, "w"), indent=1)
     print("wrote", out_prefix, "launches" if L else "", "ncu" if N else "")
