@@ -281,8 +281,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t t_lane = (qd * 32) << 16;
     uint32_t s_ph = 0, pv_ph = 0;
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-      const WorkUnit wu = wu_next;
-      if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+      const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);  // (no prefetch here: register pressure)
       for (int sub = 0; sub < wu.count; ++sub) {
         const WorkTile cur = wu.tile(sub);
         const int L = cur.L;

@@ -50,7 +50,12 @@ __device__ T block_exclusive_scan(T v, T* warp_sums, T& total) {
   return warp_prefix + x - v;
 }
 
-__device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ lengths, int32_t batch,
+// The scans, validation and longest-first lists of the whole batch, computed by one CTA.  With nparts > 1
+// (merged prelude) every CTA of the grid runs it redundantly (the batch is small), CTA `part` writes
+// the list entries of sequences b with b % nparts == part, and CTA 0 alone writes the per-batch arrays
+// (row_off, attn_off, counts, status); s_off (shared, [batch + 1]) receives the exclusive prefix of the
+// clamped lengths when non-NULL.  Returns the status word.
+__device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__ lengths, int32_t batch,
                                                                    int32_t total_tokens, int32_t heads,
                                                                    int32_t max_len, int32_t* __restrict__ row_off,
                                                                    int64_t* __restrict__ attn_off,
@@ -60,7 +65,8 @@ __device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ le
                                                                    int32_t* __restrict__ units,
                                                                    int32_t* __restrict__ unit_seq,
                                                                    int32_t* __restrict__ n_units,
-                                                                   int32_t* __restrict__ status) {
+                                                                   int32_t* __restrict__ status,
+                                                                   int part, int nparts, int32_t* s_off) {
   __shared__ int64_t ws64[32];
   __shared__ int32_t ws32[32];
   __shared__ int32_t hist[kMaxBuckets];
@@ -70,6 +76,8 @@ __device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ le
   __shared__ int32_t warp_cnt[32][kMaxBuckets];
   __shared__ int32_t s_bad;
   __shared__ unsigned long long s_raw_sum;  // sum of the raw (unclamped) lengths, for the T check
+  __shared__ int32_t s_first[kScanThreads], s_ufirst[kScanThreads];  // per sequence of the current chunk
+  __shared__ int2 s_seq[kScanThreads];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nthreads = blockDim.x, nwarps = nthreads >> 5;
@@ -107,10 +115,11 @@ __device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ le
     int64_t tot64;
     const int32_t ex32 = block_exclusive_scan<int32_t>(L, ws32, tot32);
     const int64_t ex64 = block_exclusive_scan<int64_t>(static_cast<int64_t>(L) * L, ws64, tot64);
-    if (b < batch) {
+    if (b < batch && part == 0) {
       row_off[b] = carry32 + ex32;
       attn_off[b] = carry64 + ex64;
     }
+    if (b < batch && s_off != nullptr) s_off[b] = carry32 + ex32;
     {  // bucket histogram: one shared atomic per distinct bucket per warp
       const int32_t v = (b < batch) ? (L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS : -1;
       const uint32_t same = __match_any_sync(0xffffffffu, v);
@@ -143,16 +152,18 @@ __device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ le
       carry += __shfl_sync(0xffffffffu, incl, 31);
       ucarry += __shfl_sync(0xffffffffu, uincl, 31);
     }
-    if (lane == 0) {
+    if (lane == 0 && part == 0) {
       row_off[batch] = carry32;
       attn_off[batch] = carry64;
       *status = st;
       *n_tiles = st ? 0 : carry;
       *n_units = st ? 0 : ucarry;
     }
+    if (lane == 0 && s_off != nullptr) s_off[batch] = carry32;
   }
-  if (st) return;  // data error: empty work list, nothing else is read
+  if (st) return st;  // data error: empty work list, nothing else is read
   __syncthreads();
+  const int32_t* roff = s_off != nullptr ? s_off : row_off;  // this CTA's copy of the exclusive prefix
 
   // ---- pass 2: stable rank of each sequence inside its bucket -> tile list
   for (int base = 0; base < batch; base += nthreads) {
@@ -166,23 +177,34 @@ __device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ le
     const int rank_in_warp = __popc(same & ((1u << lane) - 1u));
     if (valid && rank_in_warp == 0) warp_cnt[wid][v] = __popc(same);
     __syncthreads();
+    s_first[tid] = -1;
     if (valid && v > 0) {
       int32_t rank = running[v] + rank_in_warp;
       for (int w = 0; w < wid; ++w) rank += warp_cnt[w][v];
-      const int32_t first = bucket_base[v] + rank * heads * v;
-      const int2 seq = make_int2(row_off[b], L);
-      for (int h = 0; h < heads; ++h)
-        for (int qt = 0; qt < v; ++qt) {
-          tiles[first + h * v + qt] = b | (h << 16) | (qt << 24);
-          reinterpret_cast<int2*>(tile_seq)[first + h * v + qt] = seq;
-        }
-      const int32_t np = (v + 1) / 2;
-      const int32_t ufirst = unit_base[v] + rank * heads * np;
-      for (int h = 0; h < heads; ++h)
-        for (int qp = 0; qp < np; ++qp) {
-          units[ufirst + h * np + qp] = b | (h << 16) | (qp << 24);
-          reinterpret_cast<int2*>(unit_seq)[ufirst + h * np + qp] = seq;
-        }
+      s_first[tid] = bucket_base[v] + rank * heads * v;
+      s_ufirst[tid] = unit_base[v] + rank * heads * ((v + 1) / 2);
+      s_seq[tid] = make_int2(roff[b], L);
+    }
+    __syncthreads();
+    // each warp writes whole sequences' entries (heads * v tiles, heads * ceil(v/2) units), lanes over
+    // consecutive entries: coalesced stores instead of one thread streaming a sequence's entries alone
+    // (this CTA's sequences: b % nparts == part, spread over the warps)
+    const int j0 = (part - base % nparts + nparts) % nparts;
+    for (int j = j0 + wid * nparts; j < nthreads && base + j < batch; j += nwarps * nparts) {
+      const int32_t first = s_first[j];
+      if (first < 0) continue;
+      const int bj = base + j;
+      const int2 seq = s_seq[j];
+      const int32_t vj = (seq.y + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS, np = (vj + 1) / 2;
+      for (int k = lane; k < heads * vj; k += 32) {
+        tiles[first + k] = bj | ((k / vj) << 16) | ((k % vj) << 24);
+        reinterpret_cast<int2*>(tile_seq)[first + k] = seq;
+      }
+      const int32_t ufirst = s_ufirst[j];
+      for (int k = lane; k < heads * np; k += 32) {
+        units[ufirst + k] = bj | ((k / np) << 16) | ((k % np) << 24);
+        reinterpret_cast<int2*>(unit_seq)[ufirst + k] = seq;
+      }
     }
     __syncthreads();
     for (int u = tid; u < kMaxBuckets; u += nthreads) {
@@ -192,6 +214,7 @@ __device__ __forceinline__ void layout_scan_block(const int32_t* __restrict__ le
     }
     __syncthreads();
   }
+  return st;
 }
 
 __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t* __restrict__ lengths, int32_t batch,
@@ -206,15 +229,16 @@ __global__ void __launch_bounds__(kScanThreads) layout_scan_kernel(const int32_t
                                                                    int32_t* __restrict__ n_units,
                                                                    int32_t* __restrict__ status) {
   layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles, tile_seq, n_tiles, units,
-                    unit_seq, n_units, status);
+                    unit_seq, n_units, status, 0, 1, nullptr);
 }
 
 constexpr int kMergedMaxBatch = 8192;   // merged single-launch prelude: row_off kept in smem per block
-constexpr int kMapTokensPerBlock = 4096;
+constexpr int kSeqPerBlock = 4;   // merged prelude: sequences per CTA (lists and maps)
 
-// One launch for the whole prelude (batch <= kMergedMaxBatch): block 0 runs the scans / tile lists,
-// blocks 1.. build f_fo / f_fi for kMapTokensPerBlock tokens each, recomputing the (tiny) exclusive
-// scan of the lengths in shared memory instead of waiting for block 0.
+// One launch for the whole prelude (batch <= kMergedMaxBatch): every CTA recomputes the (small) scans
+// and bucket ranks of the whole batch in shared memory instead of waiting for one CTA to publish them,
+// then writes its share of the tile / unit lists and of f_fo / f_fi (one CTA writing every list
+// entry alone took ~15k cycles at bs 128: the store stream of a single SM, not the arithmetic, bound it).
 __global__ void __launch_bounds__(kScanThreads) layout_merged_kernel(
     const int32_t* __restrict__ lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
     int32_t* __restrict__ row_off, int64_t* __restrict__ attn_off, int32_t* __restrict__ tiles,
@@ -223,56 +247,28 @@ __global__ void __launch_bounds__(kScanThreads) layout_merged_kernel(
     int32_t* __restrict__ seq_of_tok, int32_t* __restrict__ pos_in_seq) {
   pdl_wait();  // the lengths may come from the previous kernel
   pdl_trigger();
-  if (blockIdx.x == 0) {
-    layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles, tile_seq, n_tiles,
-                      units, unit_seq, n_units, status);
-    return;
-  }
   extern __shared__ int32_t s_off[];  // [batch + 1] exclusive prefix of the (clamped) lengths
-  __shared__ int32_t ws32[32];
-  __shared__ int32_t s_bad;
-  __shared__ long long s_raw;
+  const int32_t st = layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles,
+                                       tile_seq, n_tiles, units, unit_seq, n_units, status, blockIdx.x, gridDim.x,
+                                       s_off);
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) s_bad = 0, s_raw = 0;
-  __syncthreads();
-  int32_t carry = 0;
-  for (int base = 0; base < batch; base += blockDim.x) {
-    const int b = base + tid;
-    int32_t L = b < batch ? lengths[b] : 0;
-    long long raw = L;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, o);
-    if (lane == 0 && raw != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_raw), static_cast<unsigned long long>(raw));
-    if (L < 0 || L > max_len) {
-      s_bad = 1;
-      L = L < 0 ? 0 : max_len;
-    }
-    int32_t tot;
-    const int32_t ex = block_exclusive_scan<int32_t>(L, ws32, tot);
-    if (b < batch) s_off[b] = carry + ex;
-    carry += tot;
-  }
-  if (tid == 0) s_off[batch] = carry;
-  __syncthreads();
-  const bool bad = s_bad != 0 || s_raw != total_tokens;
-  const int t0 = (blockIdx.x - 1) * kMapTokensPerBlock;
-  const int t1 = min(total_tokens, t0 + kMapTokensPerBlock);
-  for (int t = t0 + tid; t < t1; t += blockDim.x) {
-    if (bad) {
+  if (st != 0) {  // data error: the maps say "no sequence" everywhere
+    for (int t = blockIdx.x * blockDim.x + tid; t < total_tokens; t += gridDim.x * blockDim.x) {
       seq_of_tok[t] = -1;
       pos_in_seq[t] = -1;
-      continue;
     }
-    int lo = 0, hi = batch;  // invariant: s_off[lo] <= t < s_off[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= t)
-        lo = mid;
-      else
-        hi = mid;
+    return;
+  }
+  // f_fo / f_fi by sequence: warp w of the grid fills sequences w, w + n_warps, ...; lanes write
+  // consecutive tokens of a sequence (coalesced, no search)
+  const int wpb = static_cast<int>(blockDim.x) >> 5;
+  const int n_warps = gridDim.x * wpb;
+  for (int b = blockIdx.x * wpb + (tid >> 5); b < batch; b += n_warps) {
+    const int o = s_off[b], L = s_off[b + 1] - o;
+    for (int i = lane; i < L; i += 32) {
+      seq_of_tok[o + i] = b;
+      pos_in_seq[o + i] = i;
     }
-    seq_of_tok[t] = lo;
-    pos_in_seq[t] = t - s_off[lo];
   }
 }
 
@@ -308,8 +304,17 @@ void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_to
   threads = threads < 32 ? 32 : (threads > kScanThreads ? kScanThreads : threads);
   if (batch <= kMergedMaxBatch) {
     if (threads < 256) threads = 256;  // the map blocks share the block size
-    const int map_blocks = (total_tokens + kMapTokensPerBlock - 1) / kMapTokensPerBlock;
-    launch_pdl(layout_merged_kernel, dim3(1 + map_blocks), dim3(threads), sizeof(int32_t) * (batch + 1), stream, 1,
+    int blocks = (batch + kSeqPerBlock - 1) / kSeqPerBlock;
+    if (blocks > device_sm_count()) blocks = device_sm_count();
+    if (blocks < 1) blocks = 1;
+    static bool attr_set = false;  // static (~36 KB) + dynamic (up to 32 KB) smem exceeds the 48 KB default
+    if (!attr_set) {
+      if (cudaFuncSetAttribute(layout_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               sizeof(int32_t) * (kMergedMaxBatch + 1)) != cudaSuccess)
+        return;
+      attr_set = true;
+    }
+    launch_pdl(layout_merged_kernel, dim3(blocks), dim3(threads), sizeof(int32_t) * (batch + 1), stream, 1,
                lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off, L.tiles, L.tile_seq, L.n_tiles,
                L.units, L.unit_seq, L.n_units, L.status, L.seq_of_tok, L.pos_in_seq);
     return;

@@ -140,6 +140,16 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
 }
 // Asynchronous 8-byte store into another CTA's shared memory that completes `8` tx-bytes on the
 // mbarrier at bar_cluster_addr (in the same CTA as the destination) -- no fence needed by the writer.
+// gpu-scope release store / acquire load of a flag in global memory (cross-CTA handshakes)
+__device__ __forceinline__ void st_release_gpu(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_async_v2f32(uint32_t dst_cluster_addr, float a, float b, uint32_t bar_cluster_addr) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
                    dst_cluster_addr),

@@ -37,6 +37,7 @@ LAYOUT_CASES = [
     list(synth.config("C4-wiki512")[0]),
     list(synth.config("C2-mnli")[0]),
     list(synth.uniform_lengths(3000, 0, 700, seed=5)),  # > 1024 sequences: multi-chunk scan
+    list(synth.uniform_lengths(8192, 0, 40, seed=7)),   # largest merged (one-launch) prelude: 68 KB smem
     list(synth.uniform_lengths(9000, 0, 40, seed=6)),   # > 8192 sequences: two-kernel prelude
     [0],
     [],
