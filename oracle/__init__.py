@@ -25,6 +25,9 @@ Pins (tests/test_oracle_*.py, run with `-m "not gpu"`):
                 padded with src_key_padding_mask.
   flops      -- instrumented MAC counts == closed form; SPEC [2,4] -> 32/20.
   shard plan -- exhaustive search over all contiguous partitions (tiny B).
+  vgemm/trmm -- pure-Python triple loops on tiny problems (row i of trmm
+                reduces over k <= i only); identity / zero-padding cases;
+                instrumented MAC counts == the FLOP closed forms.
 No function here is "parity unpinned".
 """
 from .layout import (  # noqa: F401
@@ -55,3 +58,4 @@ from .encoder import (  # noqa: F401
 )
 from .flops import useful_flops, padded_flops, useful_macs_bruteforce, padded_macs_bruteforce, qkt_macs, causal_attention_flops  # noqa: F401
 from .shard import shard_cost, shard_plan  # noqa: F401
+from .matmul import vgemm, trmm, vgemm_flops, vgemm_padded_flops, trmm_flops  # noqa: F401

@@ -19,6 +19,8 @@ from .api import (  # noqa: F401
     ragged_attention,
     ragged_softmax,
     shard_plan,
+    trmm,
+    vgemm,
 )
 
 _lib.lib()  # load now: no silent fallback

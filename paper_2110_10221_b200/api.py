@@ -231,6 +231,36 @@ def linear_residual_layernorm(a: torch.Tensor, w: torch.Tensor, residual: torch.
     return c
 
 
+def vgemm(a: torch.Tensor, b: torch.Tensor, dims, out: Optional[torch.Tensor] = None,
+          stream=None) -> torch.Tensor:
+    """C_i = A_i B_i over padded buffers a [batch, M_max, K_max], b [batch, K_max, N_max] (bf16); dims:
+    [batch][3] host ints (M_i, N_i, K_i).  Returns c [batch, M_max, N_max]; only C_i[:M_i, :N_i] is
+    written (the rest of `out` is left as it was; a fresh `out` is zero-filled)."""
+    _need_cuda(a, b, out)
+    batch, m_max, k_max = a.shape
+    n_max = b.shape[2]
+    if b.shape[:2] != (batch, k_max) or a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
+        raise ValueError("a [batch, M_max, K_max], b [batch, K_max, N_max], bf16")
+    dh = (ctypes.c_int32 * (3 * batch))(*[int(v) for row in dims for v in row])
+    c = torch.zeros(batch, m_max, n_max, dtype=torch.bfloat16, device=a.device) if out is None else out
+    nbytes = int(C.lib().cora_vgemm_workspace_bytes(batch, dh))
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=a.device)
+    C.check(C.lib().cora_vgemm_fwd(batch, dh, _ptr(a), _ptr(b), _ptr(c), m_max, n_max, k_max, _ptr(ws), nbytes,
+                                   _stream(stream)), "cora_vgemm_fwd")
+    return c
+
+
+def trmm(l: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """c = tril(l) b (bf16; l [n, n], b [n, n_cols]); only the lower triangle of l is read."""
+    _need_cuda(l, b, out)
+    n, n_cols = b.shape
+    if l.shape != (n, n) or l.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
+        raise ValueError("l [n, n], b [n, n_cols], bf16")
+    c = torch.empty(n, n_cols, dtype=torch.bfloat16, device=b.device) if out is None else out
+    C.check(C.lib().cora_trmm_fwd(_ptr(l), _ptr(b), _ptr(c), n, n_cols, _stream(stream)), "cora_trmm_fwd")
+    return c
+
+
 def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, scale: Optional[float] = None,
                      out=None, stream=None, causal: bool = False) -> torch.Tensor:
     _need_cuda(qkv)

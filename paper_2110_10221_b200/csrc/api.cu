@@ -238,6 +238,40 @@ cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, c
   return cuda_status(launch_gemm_ln(g, as_stream(stream)));
 }
 
+size_t cora_vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host) {
+  if (batch < 0 || (batch > 0 && dims_host == nullptr)) return 0;
+  for (int i = 0; i < batch; ++i)
+    if (dims_host[3 * i] < 0 || dims_host[3 * i + 1] < 0 || dims_host[3 * i + 2] < 0) return 0;
+  return vgemm_workspace_bytes(batch, dims_host);
+}
+
+cora_status_t cora_vgemm_fwd(int32_t batch, const int32_t* dims_host, const void* a, const void* b, void* c,
+                             int32_t m_max, int32_t n_max, int32_t k_max, void* ws, size_t ws_bytes, void* stream) {
+  if (batch < 0 || m_max < 0 || n_max < 0 || k_max < 0) return CORA_ERR_INVALID;
+  if (batch == 0 || m_max == 0 || n_max == 0) return CORA_OK;
+  if (dims_host == nullptr || a == nullptr || b == nullptr || c == nullptr || ws == nullptr) return CORA_ERR_INVALID;
+  if (!aligned16(a) || !aligned16(b) || !aligned16(c) || !aligned16(ws) || (n_max % 8) != 0 || (k_max % 8) != 0 ||
+      k_max == 0)
+    return CORA_ERR_INVALID;
+  for (int i = 0; i < batch; ++i) {
+    const int32_t m = dims_host[3 * i], n = dims_host[3 * i + 1], k = dims_host[3 * i + 2];
+    if (m < 0 || n < 0 || k < 0 || m > m_max || n > n_max || k > k_max) return CORA_ERR_INVALID;
+    // a partial last k-block would read the padding of A and B unless it is the tensor's own tail
+    if ((k % 64) != 0 && k != k_max) return CORA_ERR_UNSUPPORTED;
+  }
+  if (ws_bytes < vgemm_workspace_bytes(batch, dims_host)) return CORA_ERR_INVALID;
+  return cuda_status(launch_vgemm(batch, dims_host, a, b, c, m_max, n_max, k_max, ws, as_stream(stream)));
+}
+
+cora_status_t cora_trmm_fwd(const void* l, const void* b, void* c, int32_t n, int32_t n_cols, void* stream) {
+  if (n < 0 || n_cols < 0) return CORA_ERR_INVALID;
+  if (n == 0 || n_cols == 0) return CORA_OK;
+  if (l == nullptr || b == nullptr || c == nullptr || !aligned16(l) || !aligned16(b) || !aligned16(c) ||
+      (n % 8) != 0 || (n_cols % 8) != 0)
+    return CORA_ERR_INVALID;
+  return cuda_status(launch_trmm(l, b, c, n, n_cols, as_stream(stream)));
+}
+
 cora_status_t cora_ragged_attention_fwd(const cora_layout_t* layout, const void* qkv, void* o, int32_t head_dim,
                                         float scale, void* stream) {
   if (layout == nullptr || head_dim <= 0 || head_dim > 128 || (head_dim % 2) != 0) return CORA_ERR_INVALID;

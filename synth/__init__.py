@@ -175,3 +175,11 @@ SWEEP_CONFIGS = ["C2-mnli", "C2-mrpc", "C3", "C4-wiki512", "C4-race"] + [
     f"C5-{k}-{b}" for k in ("equal", "uniform", "skewed") for b in (32, 64, 128)]
 # the 24 cells of the paper's encoder-layer table (PAPER.md:855-896, Table 4), synthetic lengths
 TABLE4_CONFIGS = [f"{ds}-{b}" for ds in DATASETS for b in (32, 64, 128)]
+
+
+def vgemm_dims(batch: int, seed: int, lo: int = 512, hi: int = 1408, step: int = 128) -> np.ndarray:
+    """[batch, 3] (M_i, N_i, K_i), each an independent uniform multiple of `step` in [lo, hi]: the vgemm
+    workload of PAPER.md:753-755 ("matrix dimensions are uniformly randomly chosen multiples of 128 in
+    [512, 1408]")."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return (rng.integers(lo // step, hi // step + 1, size=(batch, 3)) * step).astype(np.int64)
