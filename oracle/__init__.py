@@ -39,6 +39,9 @@ from .layout import (  # noqa: F401
     attn_total_size,
     tile_list,
     unit_list,
+    short_windows,
+    packed_tile_list,
+    packed_unit_list,
     n_tiles,
     validate_lengths,
     STATUS_OK,

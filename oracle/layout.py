@@ -126,6 +126,75 @@ def unit_list(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> List[Tu
     return items
 
 
+def short_windows(lengths: Sequence[int], tile: int = Q_TILE) -> List[Tuple[int, int, int]]:
+    """Windows of consecutive short sequences (SURVEY f-4; reading f4-r1 of DESIGN.md).
+
+    Sequences with 1 <= L_b <= tile occupy one q-tile each, mostly masked lanes when short (the partial
+    padding whose cost grows for short sequences).  Consecutive short sequences are
+    contiguous in the packed token array, so a 128-row window of them is one attention tile whose score
+    block is block-diagonal.  Greedy in batch order: a short sequence joins the open window if the
+    window's token count stays <= tile, else it opens a new window; a sequence longer than the tile
+    closes the open window; zero-length sequences are transparent.
+    Returns [(b_first, W tokens, n_seq)] in batch order."""
+    wins = []
+    cur = None  # [b_first, W, n_seq]
+    for b, L in enumerate(lengths):
+        L = int(L)
+        if L == 0:
+            continue
+        if L > tile:
+            if cur is not None:
+                wins.append(tuple(cur))
+                cur = None
+            continue
+        if cur is not None and cur[1] + L <= tile:
+            cur[1] += L
+            cur[2] += 1
+        else:
+            if cur is not None:
+                wins.append(tuple(cur))
+            cur = [b, L, 1]
+    if cur is not None:
+        wins.append(tuple(cur))
+    return wins
+
+
+def packed_tile_list(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> List[Tuple[int, int, int, int]]:
+    """The device work list with short-sequence packing: (b, h, qt, packed).
+
+    Sequences with more than one q-tile contribute (b, h, qt, 0) as in tile_list; the short sequences
+    contribute one item per (window, head) instead, (b_first, h, 0, n_seq >= 2).  Longest-first key
+    (-q-tiles, b, h, qt) as in tile_list (reading c15), a window keyed by its first
+    sequence.  Plain definition: enumerate, then sort."""
+    items = []
+    for b, L in enumerate(lengths):
+        if n_q_tiles(L, tile) >= 2:
+            for h in range(heads):
+                for qt in range(n_q_tiles(L, tile)):
+                    items.append((n_q_tiles(L, tile), b, h, qt, 0))
+    for b0, _w, ns in short_windows(lengths, tile):
+        for h in range(heads):
+            items.append((1, b0, h, 0, 1 if ns >= 2 else 0))
+    items.sort(key=lambda t: (-t[0], t[1], t[2], t[3]))
+    return [t[1:] for t in items]
+
+
+def packed_unit_list(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> List[Tuple[int, int, int, int]]:
+    """unit_list with the same short-sequence windows: (b, h, qp, packed)."""
+    items = []
+    for b, L in enumerate(lengths):
+        nq = n_q_tiles(L, tile)
+        if nq >= 2:
+            for h in range(heads):
+                for qp in range((nq + 1) // 2):
+                    items.append((nq, b, h, qp, 0))
+    for b0, _w, ns in short_windows(lengths, tile):
+        for h in range(heads):
+            items.append((1, b0, h, 0, 1 if ns >= 2 else 0))
+    items.sort(key=lambda t: (-t[0], t[1], t[2], t[3]))
+    return [t[1:] for t in items]
+
+
 def n_tiles(lengths: Sequence[int], heads: int, tile: int = Q_TILE) -> int:
     return heads * sum(n_q_tiles(L, tile) for L in lengths)
 

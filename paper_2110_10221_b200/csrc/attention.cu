@@ -84,15 +84,18 @@ struct AttnSmem {
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemS = 0, kTmemP = 128, kTmemO = 192;
 
-// One work tile: head h, q-tile qt of a sequence starting at packed row r0 with L tokens.
+// One work tile: head h, q-tile qt of a sequence starting at packed row r0 with L tokens -- or, packed
+// (SURVEY f-4, reading f4-r1), a window of L <= 128 consecutive tokens holding several short sequences,
+// whose score tile is block-diagonal: row i attends to the keys of its own sequence only.
 struct WorkTile {
   int h, qt, r0, L;
+  bool packed;
 };
 // Metadata of work tile idx (two independent loads: the tile word and (row_off[b], L_b)).
 __device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* tile_seq, int idx) {
   const int32_t w = __ldg(tiles + idx);
   const int2 sq = __ldg(tile_seq + idx);
-  return WorkTile{(w >> 16) & 0xFF, (w >> 24) & 0x7F, sq.x, sq.y};
+  return WorkTile{(w >> 16) & 0xFF, (w >> 24) & 0x7F, sq.x, sq.y, w < 0};
 }
 
 // The walk of one CTA: bidirectional attention visits single q-tiles of the longest-first tile list;
@@ -102,14 +105,15 @@ __device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* 
 // work-sorted list stays balanced although causal q-tiles have 1..nq KV tiles.
 struct WorkUnit {
   int h, r0, L, qt0, qt1, count;
-  __device__ __forceinline__ WorkTile tile(int sub) const { return WorkTile{h, sub ? qt1 : qt0, r0, L}; }
+  bool packed;
+  __device__ __forceinline__ WorkTile tile(int sub) const { return WorkTile{h, sub ? qt1 : qt0, r0, L, packed}; }
 };
 template <bool CAUSAL>
 __device__ __forceinline__ WorkUnit load_work(const int32_t* list, const int2* list_seq, int idx) {
   const WorkTile t = load_tile(list, list_seq, idx);
-  if (!CAUSAL) return WorkUnit{t.h, t.r0, t.L, t.qt, t.qt, 1};
+  if (!CAUSAL) return WorkUnit{t.h, t.r0, t.L, t.qt, t.qt, 1, t.packed};
   const int nq = (t.L + TQ - 1) / TQ, qp = t.qt;
-  return WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2};
+  return WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2, t.packed};
 }
 
 // CAUSAL: masked MHA (App. D.3): query i attends to keys j <= i of its sequence, so
@@ -119,7 +123,9 @@ template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
                          const int2* __restrict__ tile_seq, const int32_t* __restrict__ n_tiles_ptr,
-                         __nv_bfloat16* __restrict__ out, int32_t d_model, float scale_log2) {
+                         const int32_t* __restrict__ seq_of_tok, const int32_t* __restrict__ pos_in_seq,
+                         const int32_t* __restrict__ lengths, __nv_bfloat16* __restrict__ out, int32_t d_model,
+                         float scale_log2) {
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -328,8 +334,19 @@ __global__ void __launch_bounds__(kThreads, 2)
           float* sv = reinterpret_cast<float*>(sr);
           // row max over the valid keys (keys >= L_b masked to -inf in the tail tile; with CAUSAL also the
           // keys after the query in the diagonal tile)
-          const bool masked = (CAUSAL && j == cur.qt) || valid < TK;
-          if (CAUSAL && j == cur.qt) {
+          const bool masked = (CAUSAL && j == cur.qt) || valid < TK || cur.packed;
+          if (cur.packed) {  // block-diagonal (one KV tile: j == 0 == qt)
+            // keys [lo, hi) of the window belong to this row's sequence (f_fo / f_fi maps of the prelude)
+            int lo = 0, hi = 0;
+            if (i < L) {
+              const int t = cur.r0 + i;
+              lo = i - __ldg(pos_in_seq + t);
+              hi = lo + __ldg(lengths + __ldg(seq_of_tok + t));
+            }
+  #pragma unroll
+            for (int c = 0; c < TK; ++c)
+              if (c < lo || c >= hi || (CAUSAL && c > i)) sv[c] = -INFINITY;
+          } else if (CAUSAL && j == cur.qt) {
   #pragma unroll
             for (int c = 0; c < TK; ++c)
               if (c > i || c >= valid) sv[c] = -INFINITY;
@@ -520,11 +537,11 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
       const int ugrid = L.n_units_max < max_grid ? L.n_units_max : max_grid;
       return launch_pdl(attention_fwd_kernel<true>, dim3(ugrid > 0 ? ugrid : 1), dim3(kThreads), AttnSmem::kAlloc,
                         stream, 1, tm, L.units, reinterpret_cast<const int2*>(L.unit_seq), L.n_units,
-                        static_cast<__nv_bfloat16*>(o), d, scale_log2);
+                        L.seq_of_tok, L.pos_in_seq, L.lengths, static_cast<__nv_bfloat16*>(o), d, scale_log2);
     }
     return launch_pdl(attention_fwd_kernel<false>, dim3(grid), dim3(kThreads), AttnSmem::kAlloc, stream, 1, tm,
-                      L.tiles, reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, static_cast<__nv_bfloat16*>(o),
-                      d, scale_log2);
+                      L.tiles, reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, L.seq_of_tok, L.pos_in_seq,
+                      L.lengths, static_cast<__nv_bfloat16*>(o), d, scale_log2);
   }
   const int64_t warps = static_cast<int64_t>(L.total_tokens) * L.heads;
   const dim3 block(256), grid(static_cast<unsigned>((warps + 7) / 8));

@@ -21,6 +21,10 @@ namespace {
 
 constexpr int kScanThreads = 1024;
 constexpr int kMaxBuckets = 129;  // ceil(16383/128) + 1 distinct q-tile counts
+#ifndef CORA_PACK_MAX_BATCH
+#define CORA_PACK_MAX_BATCH 1024
+#endif
+constexpr int kPackMaxBatch = CORA_PACK_MAX_BATCH;  // short-sequence windows (merged prelude, batch <= this)
 
 template <typename T>
 __device__ T block_exclusive_scan(T v, T* warp_sums, T& total) {
@@ -78,6 +82,11 @@ __device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__
   __shared__ unsigned long long s_raw_sum;  // sum of the raw (unclamped) lengths, for the T check
   __shared__ int32_t s_first[kScanThreads], s_ufirst[kScanThreads];  // per sequence of the current chunk
   __shared__ int2 s_seq[kScanThreads];
+  // short-sequence windows (SURVEY f-4, reading f4-r1): (first sequence | packed << 31, tokens)
+  __shared__ int2 s_win[kPackMaxBatch > 0 ? kPackMaxBatch : 1];
+  __shared__ int32_t s_len[kPackMaxBatch > 0 ? kPackMaxBatch : 1];
+  __shared__ int32_t s_nwin, s_tot, s_utot;
+  const bool pack = s_off != nullptr && batch <= kPackMaxBatch && batch <= static_cast<int>(blockDim.x);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nthreads = blockDim.x, nwarps = nthreads >> 5;
@@ -120,6 +129,7 @@ __device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__
       attn_off[b] = carry64 + ex64;
     }
     if (b < batch && s_off != nullptr) s_off[b] = carry32 + ex32;
+    if (b < batch && pack) s_len[b] = L;
     {  // bucket histogram: one shared atomic per distinct bucket per warp
       const int32_t v = (b < batch) ? (L + CORA_TILE_ROWS - 1) / CORA_TILE_ROWS : -1;
       const uint32_t same = __match_any_sync(0xffffffffu, v);
@@ -152,17 +162,65 @@ __device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__
       carry += __shfl_sync(0xffffffffu, incl, 31);
       ucarry += __shfl_sync(0xffffffffu, uincl, 31);
     }
-    if (lane == 0 && part == 0) {
-      row_off[batch] = carry32;
-      attn_off[batch] = carry64;
-      *status = st;
-      *n_tiles = st ? 0 : carry;
-      *n_units = st ? 0 : ucarry;
-    }
+    if (lane == 0) s_tot = carry, s_utot = ucarry;
     if (lane == 0 && s_off != nullptr) s_off[batch] = carry32;
   }
-  if (st) return st;  // data error: empty work list, nothing else is read
   __syncthreads();
+  if (pack) {
+    // Greedy windows in batch order (oracle.short_windows), computed in parallel (one sequence per
+    // thread, batch <= blockDim): a window opened by short sequence b (1 <= L <= 128) takes every
+    // following sequence until the first one that overflows 128 tokens, end(b) (a long sequence always
+    // does; zero-length ones never do) -- a binary search over the prefix sums.  The windows are the
+    // short sequences on the chain 0 -> nxt -> nxt ... with nxt(b) = end(b) for a short b and b + 1
+    // otherwise; the chain is marked by pointer doubling (ceil(log2 batch) rounds).
+    int32_t* jmp = s_first;   // scratch: pass 2 reuses these arrays afterwards
+    int32_t* on = s_ufirst;
+    const int b = tid;
+    int32_t Lb = 0, end = batch;
+    if (b < batch) {
+      Lb = s_len[b];
+      if (Lb >= 1 && Lb <= CORA_TILE_ROWS) {
+        int lo = b + 1, hi = batch;  // end = first j in [b+1, batch) with off[j+1] - off[b] > 128
+        const int base_off = s_off[b];
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_off[mid + 1] - base_off > CORA_TILE_ROWS) hi = mid; else lo = mid + 1;
+        }
+        end = lo;
+        jmp[b] = end;
+      } else {
+        jmp[b] = b + 1;
+      }
+      on[b] = b == 0;
+    }
+    __syncthreads();
+    for (int span = 1; span < batch; span <<= 1) {
+      const int nb = b < batch ? jmp[b] : batch;
+      if (b < batch && on[b] && nb < batch) on[nb] = 1;
+      const int nn = (b < batch && nb < batch) ? jmp[nb] : batch;
+      __syncthreads();
+      if (b < batch) jmp[b] = nn;
+      __syncthreads();
+    }
+    const bool start = b < batch && on[b] && Lb >= 1 && Lb <= CORA_TILE_ROWS;
+    int32_t n_win;
+    const int32_t idx = block_exclusive_scan<int32_t>(start ? 1 : 0, ws32, n_win);
+    if (start) {
+      const int32_t W = s_off[end] - s_off[b];
+      s_win[idx] = make_int2(b | (W > Lb ? static_cast<int>(0x80000000u) : 0), W);
+    }
+    if (tid == 0) s_nwin = n_win;
+  }
+  __syncthreads();
+  if (tid == 0 && part == 0) {
+    row_off[batch] = carry32;
+    attn_off[batch] = carry64;
+    *status = st;
+    // packed: the one-tile sequences' heads * hist[1] entries become heads * (windows) entries
+    *n_tiles = st ? 0 : (pack ? bucket_base[1] + heads * s_nwin : s_tot);
+    *n_units = st ? 0 : (pack ? unit_base[1] + heads * s_nwin : s_utot);
+  }
+  if (st) return st;  // data error: empty work list, nothing else is read
   const int32_t* roff = s_off != nullptr ? s_off : row_off;  // this CTA's copy of the exclusive prefix
 
   // ---- pass 2: stable rank of each sequence inside its bucket -> tile list
@@ -178,7 +236,7 @@ __device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__
     if (valid && rank_in_warp == 0) warp_cnt[wid][v] = __popc(same);
     __syncthreads();
     s_first[tid] = -1;
-    if (valid && v > 0) {
+    if (valid && v > (pack ? 1 : 0)) {
       int32_t rank = running[v] + rank_in_warp;
       for (int w = 0; w < wid; ++w) rank += warp_cnt[w][v];
       s_first[tid] = bucket_base[v] + rank * heads * v;
@@ -213,6 +271,23 @@ __device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__
       running[u] += s;
     }
     __syncthreads();
+  }
+  if (pack) {
+    // window entries (this CTA's windows: w % nparts == part), one per (window, head), after the
+    // multi-tile sequences' entries, ordered (first sequence, head) like every other bucket
+    const int nw = s_nwin;
+    for (int w = part + wid * nparts; w < nw; w += nwarps * nparts) {
+      const int2 win = s_win[w];
+      const int b0 = win.x & 0x7FFFFFFF;
+      const int2 seq = make_int2(roff[b0], win.y);
+      for (int k = lane; k < heads; k += 32) {
+        const int32_t word = win.x | (k << 16);
+        tiles[bucket_base[1] + w * heads + k] = word;
+        reinterpret_cast<int2*>(tile_seq)[bucket_base[1] + w * heads + k] = seq;
+        units[unit_base[1] + w * heads + k] = word;
+        reinterpret_cast<int2*>(unit_seq)[unit_base[1] + w * heads + k] = seq;
+      }
+    }
   }
   return st;
 }

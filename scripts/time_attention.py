@@ -13,6 +13,14 @@ import numpy as np
 import torch
 
 import synth
+
+
+def _config(name):
+    """synth.config names, or ds:<dataset>:<batch> (Table 3 length generator, d 512 / 8 heads / 2048)."""
+    if name.startswith("ds:"):
+        _, ds, bs = name.split(":")
+        return synth.dataset_lengths(ds, int(bs)), 512, 8, 2048
+    return synth.config(name)
 import paper_2110_10221_b200 as P
 
 cfgs = (sys.argv[1] if len(sys.argv) > 1 else "C4-wiki512").split(",")
@@ -37,7 +45,7 @@ for cfg in cfgs:
         ln, bs = cfg[1:].split("x")
         lengths, d, H = np.full(int(bs), int(ln), dtype=np.int64), 512, 8
     else:
-        lengths, d, H, _ = synth.config(cfg)
+        lengths, d, H, _ = _config(cfg)
     T = int(lengths.sum())
     qkv = torch.randn(T, 3 * d, device="cuda").to(torch.bfloat16)
     lay = P.layout_build(torch.tensor(lengths, dtype=torch.int32, device="cuda"), T, H, 512)

@@ -12,11 +12,19 @@ import numpy as np
 import torch
 
 import synth
+
+
+def _config(name):
+    """synth.config names, or ds:<dataset>:<batch> (Table 3 length generator, d 512 / 8 heads / 2048)."""
+    if name.startswith("ds:"):
+        _, ds, bs = name.split(":")
+        return synth.dataset_lengths(ds, int(bs)), 512, 8, 2048
+    return synth.config(name)
 import paper_2110_10221_b200 as P
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4-wiki512"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
-lengths, d, H, dff = synth.config(cfg)
+lengths, d, H, dff = _config(cfg)
 T = int(lengths.sum())
 w = synth.encoder_weights(d, H, dff)
 params = P.EncoderParams.from_host(w)

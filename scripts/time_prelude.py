@@ -11,10 +11,18 @@ sys.path.insert(0, ROOT)
 import torch
 
 import synth
+
+
+def _config(name):
+    """synth.config names, or ds:<dataset>:<batch> (Table 3 length generator, d 512 / 8 heads / 2048)."""
+    if name.startswith("ds:"):
+        _, ds, bs = name.split(":")
+        return synth.dataset_lengths(ds, int(bs)), 512, 8, 2048
+    return synth.config(name)
 import paper_2110_10221_b200 as P
 
 for cfg in (sys.argv[1] if len(sys.argv) > 1 else "C4-wiki512,C2-mnli").split(","):
-    lengths = synth.config(cfg)[0]
+    lengths = _config(cfg)[0]
     L = torch.tensor(lengths, dtype=torch.int32, device="cuda")
     T = int(lengths.sum())
     lay = P.layout_build(L, T, 8, 512)

@@ -142,3 +142,49 @@ def test_unit_list_alternative_derivation(seed):
     # every q-tile of the tile list is covered by exactly one unit (qt // 2 == qp)
     covered = sorted((b, h, qt) for b, h, qp in expect for qt in (2 * qp, 2 * qp + 1) if qt < nq[b])
     assert covered == sorted(oracle.tile_list(L, H))
+
+
+def test_short_windows_examples():
+    # tile 8 for readability: [3,4 | 2,2,2 | 9 | 5 | 0 ignored, 1] -> greedy windows in batch order
+    L = [3, 4, 2, 2, 2, 9, 5, 0, 1]
+    assert oracle.short_windows(L, tile=8) == [(0, 7, 2), (2, 6, 3), (6, 6, 2)]
+    assert oracle.short_windows([], tile=8) == []
+    assert oracle.short_windows([0, 0], tile=8) == []
+    assert oracle.short_windows([8, 8], tile=8) == [(0, 8, 1), (1, 8, 1)]   # full tiles never merge
+    assert oracle.short_windows([9, 1, 9], tile=8) == [(1, 1, 1)]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_short_windows_invariants(seed):
+    rng = np.random.default_rng(seed)
+    L = [int(x) for x in rng.integers(0, 300, size=60)]
+    ro = oracle.row_offsets(L)
+    wins = oracle.short_windows(L)
+    covered = []
+    for b0, W, ns in wins:
+        members = [b for b in range(b0, len(L)) if L[b] > 0][:ns]
+        assert all(1 <= L[b] <= 128 for b in members)
+        assert sum(L[b] for b in members) == W <= 128
+        # contiguous in the packed token array: the members' rows are [ro[b0], ro[b0] + W)
+        assert ro[members[-1]] + L[members[-1]] == ro[b0] + W
+        covered += members
+    assert covered == [b for b in range(len(L)) if 1 <= L[b] <= 128]  # every short sequence, once, in order
+    # greedy maximality: the next short sequence after a window did not fit (or a long one intervened)
+    for (b0, W, ns), nxt in zip(wins, wins[1:]):
+        b1 = nxt[0]
+        between = [b for b in range(b0, b1) if L[b] > 128]
+        assert between or W + L[b1] > 128
+
+
+def test_packed_lists_cover_the_same_rows():
+    rng = np.random.default_rng(7)
+    L = [int(x) for x in rng.integers(0, 400, size=40)]
+    H = 3
+    pt = oracle.packed_tile_list(L, H)
+    plain = oracle.tile_list(L, H)
+    long_items = [(b, h, qt) for b, h, qt, _p in pt if oracle.layout.n_q_tiles(L[b]) >= 2]
+    assert long_items == [t for t in plain if oracle.layout.n_q_tiles(L[t[0]]) >= 2]
+    n_win = len(oracle.short_windows(L))
+    assert len(pt) == len(long_items) + H * n_win
+    pu = oracle.packed_unit_list(L, H)
+    assert len(pu) == len([u for u in oracle.unit_list(L, H) if oracle.layout.n_q_tiles(L[u[0]]) >= 2]) + H * n_win
