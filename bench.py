@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-stack", action="store_true", help="skip the 6-layer stack measurement")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     args = ap.parse_args()
@@ -351,6 +352,33 @@ def main():
     else:
         ms = ms_local
 
+    # ---------------------------------------------------------------- the paper's 6-layer model (SURVEY f-4)
+    # one layout (prelude) per batch shared by 6 layers, one CUDA graph per
+    # step, L2 flushed between steps like the headline number; reported beside it, not instead of it
+    stack = None
+    if not args.no_stack and T_loc and world == 1:
+        stack_params = [P.EncoderParams.from_host(synth.encoder_weights(d, H, dff, seed=200 + i), device=dev)
+                        for i in range(6)]
+        enc_stack = P.EncoderStack(stack_params)
+        y_stack = torch.empty_like(y_dev)
+
+        def stack_step():
+            enc_stack(x_dev, P.layout_build(len_dev, T_loc, H, 512), out=y_stack)
+
+        stack_step()
+        torch.cuda.synchronize()
+        g_stack = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_stack):
+            stack_step()
+        for _ in range(args.warmup):
+            g_stack.replay()
+        torch.cuda.synchronize()
+        n_stack = max(3, min(args.steps, 50))
+        st_ms = float(np.mean(timed(g_stack.replay, n_stack)))
+        stack = {"layers": 6, "ms_per_step": st_ms, "steps": n_stack,
+                 "value": 6 * useful_flops(lengths, d, dff) / (st_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                 "step": "prelude(a1) once + 6 encoder layers, one CUDA graph"}
+
     # ---------------------------------------------------------------- e2e: host buffers through the C ABI
     e2e = None
     if not args.no_e2e and T_loc:
@@ -453,6 +481,7 @@ def main():
         "roofline": roofline,
         "kernels": kernels,
         "prelude_ms": prelude_ms,
+        "stack6": stack,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": (1 + layer_launches) * args.steps,

@@ -174,6 +174,18 @@ int32_t cora_encoder_layer_launches(const cora_encoder_params_t* p, int32_t tota
 cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
                                         void* y, void* ws, size_t ws_bytes, void* stream, void* const* events);
 
+/* Workspace for cora_encoder_stack_fwd: the largest layer workspace + one [T, d_model] bf16 buffer
+ * (n_layers > 1); 0 on invalid arguments. */
+size_t cora_encoder_stack_workspace_bytes(const cora_encoder_params_t* layers, int32_t n_layers, int32_t total_tokens);
+
+/* y = layer_{n-1}( ... layer_0(x)) over one ragged batch: a stack of encoder layers (the paper's 6-layer
+ * model) sharing ONE layout -- the prelude runs once per batch, not per layer, as the
+ * raggedness is the same for every layer (SURVEY f-4).  layers: n_layers parameter
+ * structs (same d_model and heads); activations ping-pong between y and a workspace buffer (x is only
+ * read; x and y must not alias).  Same validation and errors as cora_encoder_layer_fwd. */
+cora_status_t cora_encoder_stack_fwd(const cora_encoder_params_t* layers, int32_t n_layers, const cora_layout_t* layout,
+                                     const void* x, void* y, void* ws, size_t ws_bytes, void* stream);
+
 /* Workspace for cora_encoder_forward_host (device lengths + X + Y + layout tables + layer workspace). */
 size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
                                          int32_t max_len);

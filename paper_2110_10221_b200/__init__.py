@@ -8,6 +8,7 @@ from . import _lib
 from .api import (  # noqa: F401
     EncoderLayer,
     EncoderParams,
+    EncoderStack,
     HostForward,
     RaggedLayout,
     build_info,

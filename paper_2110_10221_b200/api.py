@@ -175,6 +175,31 @@ class EncoderLayer:
         return y
 
 
+class EncoderStack:
+    """n encoder layers over one ragged batch sharing ONE layout (cora_encoder_stack_fwd): the prelude
+    runs once per batch, the layers ping-pong between the output and a workspace buffer."""
+
+    def __init__(self, params: Sequence[EncoderParams]):
+        self.params = list(params)
+        self.cps = (C.EncoderParams * len(self.params))(*[p.cstruct() for p in self.params])
+        self.ws = None
+
+    def __call__(self, x: torch.Tensor, layout: RaggedLayout, out: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+        _need_cuda(x, out)
+        T = layout.total_tokens
+        if x.dtype != torch.bfloat16 or x.shape != (T, self.params[0].d_model):
+            raise ValueError("x must be bf16 [T, d_model]")
+        n = len(self.params)
+        nbytes = int(C.lib().cora_encoder_stack_workspace_bytes(self.cps, n, T))
+        if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
+            self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)
+        y = torch.empty_like(x) if out is None else out
+        C.check(C.lib().cora_encoder_stack_fwd(self.cps, n, ctypes.byref(layout.c), _ptr(x), _ptr(y), _ptr(self.ws),
+                                               self.ws.numel(), _stream(stream)), "cora_encoder_stack_fwd")
+        return y
+
+
 class HostForward:
     """End-to-end public call with HOST buffers (cora_encoder_forward_host): H2D of lengths and x,
     device prelude, the layer, D2H of y -- one C call, enqueued on the stream."""

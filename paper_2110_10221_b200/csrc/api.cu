@@ -410,6 +410,46 @@ cora_status_t cora_encoder_layer_fwd(const cora_encoder_params_t* p, const cora_
   return cora_encoder_layer_fwd_ex(p, layout, x, y, ws, ws_bytes, stream, nullptr);
 }
 
+size_t cora_encoder_stack_workspace_bytes(const cora_encoder_params_t* layers, int32_t n_layers, int32_t total_tokens) {
+  if (layers == nullptr || n_layers < 1 || total_tokens < 0) return 0;
+  size_t layer_ws = 0;
+  for (int i = 0; i < n_layers; ++i) {
+    const size_t b = carve_encoder(&layers[i], total_tokens).total;
+    if (b > layer_ws) layer_ws = b;
+  }
+  // + one [T, d] activation buffer: the layers ping-pong between it and y
+  return layer_ws + (n_layers > 1 ? align_up(2ull * static_cast<size_t>(total_tokens) * layers[0].d_model) : 0);
+}
+
+cora_status_t cora_encoder_stack_fwd(const cora_encoder_params_t* layers, int32_t n_layers, const cora_layout_t* layout,
+                                     const void* x, void* y, void* ws, size_t ws_bytes, void* stream) {
+  if (layers == nullptr || layout == nullptr || n_layers < 1) return CORA_ERR_INVALID;
+  for (int i = 1; i < n_layers; ++i)
+    if (layers[i].d_model != layers[0].d_model || layers[i].heads != layers[0].heads) return CORA_ERR_INVALID;
+  const int32_t T = layout->total_tokens;
+  const size_t need = cora_encoder_stack_workspace_bytes(layers, n_layers, T);
+  if (need == 0 || ws == nullptr || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
+    return CORA_ERR_INVALID;
+  if (T == 0 || layout->batch == 0) return CORA_OK;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  void* tmp = nullptr;
+  if (n_layers > 1) {
+    tmp = w;
+    w += align_up(2ull * static_cast<size_t>(T) * layers[0].d_model);
+  }
+  const size_t layer_ws = ws_bytes - static_cast<size_t>(w - static_cast<uint8_t*>(ws));
+  // layer i writes y when (n_layers - 1 - i) is even, else tmp, so the last layer lands in y and no layer
+  // reads and writes the same buffer
+  const void* in = x;
+  for (int i = 0; i < n_layers; ++i) {
+    void* out = ((n_layers - 1 - i) % 2 == 0) ? y : tmp;
+    const cora_status_t st = cora_encoder_layer_fwd_ex(&layers[i], layout, in, out, w, layer_ws, stream, nullptr);
+    if (st != CORA_OK) return st;
+    in = out;
+  }
+  return CORA_OK;
+}
+
 size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
                                          int32_t max_len) {
   if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return 0;

@@ -344,3 +344,32 @@ def test_layer_events_and_user_stream():
     ref = layer(x, _layout(lengths, H))
     assert torch.equal(y, ref)
     assert all(ev[i].elapsed_time(ev[i + 1]) >= 0 for i in range(7))
+
+
+# ---------------------------------------------------------------- layer stack (SURVEY f-4)
+@pytest.mark.parametrize("n_layers,lengths,d,H,dff", [
+    (6, [3, 130, 1, 64, 0, 257], 512, 8, 2048),   # the paper's 6-layer model dims
+    (3, list(synth.C1_LENGTHS), 16, 2, 32),       # C1 dims (SIMT attention)
+    (1, [5, 9], 512, 8, 2048),
+])
+def test_encoder_stack(n_layers, lengths, d, H, dff):
+    ws = [synth.encoder_weights(d, H, dff, seed=100 + i) for i in range(n_layers)]
+    x = synth.activations(int(np.sum(lengths)), d)
+    params = [P().EncoderParams.from_host(w) for w in ws]
+    lay = _layout(lengths, H)  # ONE layout for the whole stack
+    y = P().EncoderStack(params)(bf16_cuda(x), lay)
+    # the oracle chains its own layers, rounding each layer's output to bf16: the storage point of the
+    # layer output (reading c13)
+    ref = x
+    for w in ws:
+        ref = synth.round_bf16(oracle.encoder_layer(ref, lengths, w))
+    # tolerance: the one-layer bound per layer -- the bf16 storage-point errors of successive layers add
+    # to first order (reading s2 of DESIGN.md)
+    err = rel_err(to_np(y), ref)
+    print(f"stack n={n_layers} rel_err={err:.3e}")
+    assert err <= TOL_BF16 * n_layers
+    # and equals the single-layer calls chained on the GPU, bitwise
+    z = bf16_cuda(x)
+    for p in params:
+        z = P().encoder_layer(z, lay, p)
+    assert torch.equal(y, z)
