@@ -74,7 +74,8 @@ struct AttnSmem {
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + QSTAGES * kTileBytes;
   static constexpr int kOffV = kOffK + KSTAGES * kTileBytes;
-  static constexpr int kOffBar = kOffV + VSTAGES * kTileBytes;
+  static constexpr int kOffMeta = kOffV + VSTAGES * kTileBytes;  // int4 [4 softmax warps][2 slots]
+  static constexpr int kOffBar = kOffMeta + 4 * 2 * 16;
   // q_full/empty[QS], k_full/empty[KS], v_full/empty[VS], s_full, s_empty, p_full, pv_done, o_empty
   static constexpr int kNumBars = 2 * (QSTAGES + KSTAGES + VSTAGES) + 5;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
@@ -286,8 +287,34 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int i = qd * 32 + lane;  // query row within the tile
     const uint32_t t_lane = (qd * 32) << 16;
     uint32_t s_ph = 0, pv_ph = 0;
-    for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-      const WorkUnit wu = load_work<CAUSAL>(tiles, tile_seq, idx);  // (no prefetch here: register pressure)
+    // the next tile's metadata is prefetched one tile ahead into shared memory with cp.async (no
+    // registers held while in flight; prefetching into registers spilled)
+    int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + (warp - 2) * 2;  // [2 slots] per warp
+    auto prefetch_meta = [&](int idx, int slot) {
+      if (lane == 0 && idx < n_tiles) {
+        cp_async_4(&meta[slot].x, tiles + idx);
+        cp_async_8(&meta[slot].z, tile_seq + idx);
+      }
+      cp_async_commit();
+    };
+    int slot = 0;
+    prefetch_meta(blockIdx.x, 0);
+    for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x, slot ^= 1) {
+      cp_async_wait_all();
+      __syncwarp();
+      const int4 mt = meta[slot];
+      __syncwarp();
+      prefetch_meta(idx + gridDim.x, slot ^ 1);
+      WorkUnit wu;
+      {
+        const WorkTile t{(mt.x >> 16) & 0xFF, (mt.x >> 24) & 0x7F, mt.z, mt.w, mt.x < 0};
+        if (!CAUSAL) {
+          wu = WorkUnit{t.h, t.r0, t.L, t.qt, t.qt, 1, t.packed};
+        } else {
+          const int nq = (t.L + TQ - 1) / TQ, qp = t.qt;
+          wu = WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2, t.packed};
+        }
+      }
       for (int sub = 0; sub < wu.count; ++sub) {
         const WorkTile cur = wu.tile(sub);
         const int L = cur.L;
