@@ -192,10 +192,17 @@ size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t
 
 /* End-to-end call with HOST buffers: copies lengths_host[batch] (int32) and x_host[T, d] (bf16)
  * host->device, builds the layout (step a1), runs the layer (a2..a8) and copies y_host[T, d] back,
- * all enqueued on `stream` (asynchronous when the host buffers are pinned; the caller synchronises
- * the stream before reading y_host).  The device status word is not read (no hidden sync): call
- * cora_layout_status on *layout_out after synchronising to detect data errors.  layout_out may be
- * NULL.  T = total_tokens must equal sum(lengths_host) (checked on the device). */
+ * all ordered after prior work on `stream` and before later work on it (asynchronous when the host
+ * buffers are pinned; the caller synchronises the stream before reading y_host).  For T >= 8192 the
+ * batch is cut (on the host, from lengths_host) into 4 (T >= 16384: 8) contiguous sequence ranges that
+ * are copied in, computed and copied out as a pipeline over the caller's stream and two library-owned
+ * side streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the layer on chunk c); each chunk is a
+ * ragged batch of its own, so every row is computed exactly as in the one-shot path.  The side streams
+ * and events are created once per device; concurrent calls from several host threads on one device are
+ * not supported.  The device status word is not read (no hidden sync): call cora_layout_status on
+ * *layout_out (the whole batch's layout, built on `stream`) after synchronising to detect data errors
+ * (invalid lengths also disable the chunking).  layout_out may be NULL (then no whole-batch layout is
+ * built when chunking).  T = total_tokens must equal sum(lengths_host). */
 cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
                                         int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host,
                                         void* ws, size_t ws_bytes, cora_layout_t* layout_out, void* stream);

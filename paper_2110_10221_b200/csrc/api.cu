@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -454,9 +455,42 @@ size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t
                                          int32_t max_len) {
   if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return 0;
   const size_t xy = align_up(2ull * static_cast<size_t>(total_tokens) * p->d_model);
+  // lengths + x + y + the whole batch's layout (layout_out) + one chunk layout + the layer workspace
   return align_up(sizeof(int32_t) * (batch + 1)) + 2 * xy +
-         cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len) + carve_encoder(p, total_tokens).total;
+         2 * cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len) + carve_encoder(p, total_tokens).total;
 }
+
+namespace {
+// Side streams and events of the pipelined host forward, created once per device (never on the hot path
+// after the first call).
+constexpr int kMaxChunks = 8;
+struct HostPipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr, h2d_ev[kMaxChunks] = {}, comp_ev[kMaxChunks] = {};
+  bool ok = false;
+};
+HostPipe g_pipe[64];
+std::mutex g_pipe_mu;
+
+HostPipe* host_pipe() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  HostPipe& hp = g_pipe[dev];
+  if (!hp.ok) {
+    bool good = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&hp.done, cudaEventDisableTiming) == cudaSuccess;
+    for (int c = 0; good && c < kMaxChunks; ++c)
+      good = cudaEventCreateWithFlags(&hp.h2d_ev[c], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&hp.comp_ev[c], cudaEventDisableTiming) == cudaSuccess;
+    if (!good) return nullptr;
+    hp.ok = true;
+  }
+  return &hp;
+}
+}  // namespace
 
 cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
                                         int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host,
@@ -467,29 +501,106 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
   if (total_tokens > 0 && (x_host == nullptr || y_host == nullptr)) return CORA_ERR_INVALID;
   const size_t need = cora_forward_host_workspace_bytes(p, batch, total_tokens, max_len);
   if (need == 0 || ws_bytes < need) return CORA_ERR_INVALID;
-  const size_t xbytes = 2ull * static_cast<size_t>(total_tokens) * p->d_model;
+  const int32_t d = p->d_model;
+  const size_t xbytes = 2ull * static_cast<size_t>(total_tokens) * d;
   const size_t xy = align_up(xbytes);
   uint8_t* w = static_cast<uint8_t*>(ws);
   int32_t* d_len = reinterpret_cast<int32_t*>(w);
   w += align_up(sizeof(int32_t) * (batch + 1));
-  void* d_x = w;
+  uint8_t* d_x = w;
   w += xy;
-  void* d_y = w;
+  uint8_t* d_y = w;
   w += xy;
   const size_t lay_bytes = cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len);
-  void* lay_ws = w;
+  void* lay_ws = w;  // the whole batch's layout (layout_out)
   w += lay_bytes;
+  void* chunk_lay_ws = w;  // the current chunk's layout
+  w += lay_bytes;
+  const size_t layer_ws = ws_bytes - static_cast<size_t>(w - static_cast<uint8_t*>(ws));
   cudaStream_t s = as_stream(stream);
+
+  // The lengths are on the host: chunk the batch there.  K contiguous sequence ranges of ~T/K tokens
+  // each are copied in, computed and copied out as a pipeline over three streams (H2D of chunk c+1 and
+  // D2H of chunk c-1 overlap the layer on chunk c; PCIe is full duplex): sequences are independent, so
+  // a chunk is a ragged batch of its own (its layout rebased to its first token).
+  int64_t sum = 0;
+  bool bad = false;
+  for (int b = 0; b < batch; ++b) {
+    sum += lengths_host[b];
+    bad |= lengths_host[b] < 0 || lengths_host[b] > max_len;
+  }
+  int K = (bad || sum != total_tokens) ? 1 : total_tokens >= 16384 ? 8 : total_tokens >= 8192 ? 4 : 1;
+  if (const char* e = getenv("CORA_HOST_CHUNKS")) {  // experiments: force the chunk count (1..8)
+    const int k = atoi(e);
+    if (k >= 1 && k <= kMaxChunks && !bad && sum == total_tokens) K = k;
+  }
+  if (K > batch) K = batch > 0 ? batch : 1;
+  int32_t seq_begin[kMaxChunks + 1], tok_begin[kMaxChunks + 1];
+  seq_begin[0] = 0, tok_begin[0] = 0;
+  {
+    int b = 0;
+    int64_t acc = 0;
+    for (int c = 1; c < K; ++c) {
+      const int64_t target = static_cast<int64_t>(total_tokens) * c / K;
+      while (b < batch && acc + lengths_host[b] <= target) acc += lengths_host[b++];
+      seq_begin[c] = b, tok_begin[c] = static_cast<int32_t>(acc);
+    }
+    seq_begin[K] = batch, tok_begin[K] = total_tokens;
+  }
+  HostPipe* hp = K > 1 ? host_pipe() : nullptr;
+  if (hp == nullptr) K = 1, seq_begin[1] = batch, tok_begin[1] = total_tokens;
+
   if (batch > 0 && cudaMemcpyAsync(d_len, lengths_host, sizeof(int32_t) * batch, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return CORA_ERR_CUDA;
-  if (xbytes > 0 && cudaMemcpyAsync(d_x, x_host, xbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return CORA_ERR_CUDA;
-  cora_layout_t L;
-  cora_status_t st = cora_layout_build(d_len, batch, total_tokens, p->heads, max_len, lay_ws, lay_bytes, &L, stream);
-  if (st != CORA_OK) return st;
-  if (layout_out != nullptr) *layout_out = L;
-  st = cora_encoder_layer_fwd_ex(p, &L, d_x, d_y, w, ws_bytes - (w - static_cast<uint8_t*>(ws)), stream, nullptr);
-  if (st != CORA_OK) return st;
-  if (xbytes > 0 && cudaMemcpyAsync(y_host, d_y, xbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return CORA_ERR_CUDA;
+  if (layout_out != nullptr || K == 1) {
+    // the whole batch's layout: the status word checks sum L == T and 0 <= L <= max_len on the device
+    cora_layout_t L;
+    const cora_status_t st = cora_layout_build(d_len, batch, total_tokens, p->heads, max_len, lay_ws, lay_bytes, &L, stream);
+    if (st != CORA_OK) return st;
+    if (layout_out != nullptr) *layout_out = L;
+    if (K == 1) {
+      if (xbytes > 0 && cudaMemcpyAsync(d_x, x_host, xbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return CORA_ERR_CUDA;
+      const cora_status_t st2 = cora_encoder_layer_fwd_ex(p, &L, d_x, d_y, w, layer_ws, stream, nullptr);
+      if (st2 != CORA_OK) return st2;
+      if (xbytes > 0 && cudaMemcpyAsync(y_host, d_y, xbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return CORA_ERR_CUDA;
+      return CORA_OK;
+    }
+  }
+  // pipelined: fork the side streams off the caller's stream, join them back at the end
+  if (cudaEventRecord(hp->start, s) != cudaSuccess || cudaStreamWaitEvent(hp->h2d, hp->start, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(hp->d2h, hp->start, 0) != cudaSuccess)
+    return CORA_ERR_CUDA;
+  const size_t row = 2ull * d;
+  for (int c = 0; c < K; ++c) {
+    const size_t off = row * tok_begin[c], bytes = row * (tok_begin[c + 1] - tok_begin[c]);
+    if (bytes > 0 && cudaMemcpyAsync(d_x + off, static_cast<const uint8_t*>(x_host) + off, bytes,
+                                     cudaMemcpyHostToDevice, hp->h2d) != cudaSuccess)
+      return CORA_ERR_CUDA;
+    if (cudaEventRecord(hp->h2d_ev[c], hp->h2d) != cudaSuccess) return CORA_ERR_CUDA;
+  }
+  for (int c = 0; c < K; ++c) {
+    const int32_t nb = seq_begin[c + 1] - seq_begin[c], nt = tok_begin[c + 1] - tok_begin[c];
+    if (cudaStreamWaitEvent(s, hp->h2d_ev[c], 0) != cudaSuccess) return CORA_ERR_CUDA;
+    if (nt > 0) {
+      cora_layout_t Lc;
+      cora_status_t st = cora_layout_build(d_len + seq_begin[c], nb, nt, p->heads, max_len, chunk_lay_ws, lay_bytes,
+                                           &Lc, stream);
+      if (st != CORA_OK) return st;
+      st = cora_encoder_layer_fwd_ex(p, &Lc, d_x + row * tok_begin[c], d_y + row * tok_begin[c], w, layer_ws, stream,
+                                     nullptr);
+      if (st != CORA_OK) return st;
+    }
+    if (cudaEventRecord(hp->comp_ev[c], s) != cudaSuccess) return CORA_ERR_CUDA;
+    if (cudaStreamWaitEvent(hp->d2h, hp->comp_ev[c], 0) != cudaSuccess) return CORA_ERR_CUDA;
+    const size_t off = row * tok_begin[c], bytes = row * nt;
+    if (bytes > 0 && cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + off, d_y + off, bytes, cudaMemcpyDeviceToHost,
+                                     hp->d2h) != cudaSuccess)
+      return CORA_ERR_CUDA;
+  }
+  if (cudaEventRecord(hp->done, hp->d2h) != cudaSuccess || cudaStreamWaitEvent(s, hp->done, 0) != cudaSuccess)
+    return CORA_ERR_CUDA;
   return CORA_OK;
 }
 
