@@ -38,7 +38,10 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiRows = 32;                      // rows per epilogue warp
 constexpr int kEpiBufBytes = kEpiRows * BK * 2;   // 4 KB staging buffer (32 rows x 128 B)
 
-template <int BN, int STAGES, int CL, bool LN>
+// NBUF: staging buffers per epilogue warp -- one per 64-column chunk when a residual is TMA-prefetched into
+// them (RESIDUAL / LN), else one reused buffer, which frees 32 KB for a sixth pipeline stage (the mainloop
+// is bound by the bytes in flight: stages x stage bytes / TMA latency)
+template <int BN, int STAGES, int CL, bool LN, int NBUF = 2>
 struct GemmSmem {
   static constexpr int kChunks = BN / BK;             // 64-column epilogue chunks per tile
   static constexpr int kWarpCols = BN / 2;            // columns per epilogue warp
@@ -48,8 +51,9 @@ struct GemmSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + STAGES * kABytes;
-  static constexpr int kOffC = kOffB + STAGES * kBBytes;  // per warp: kBufs staging buffers
-  static constexpr int kOffBias = kOffC + kEpiWarps * kBufs * kEpiBufBytes;  // per warp: kWarpCols bf16
+  static constexpr int kNBuf = NBUF;
+  static constexpr int kOffC = kOffB + STAGES * kBBytes;  // per warp: NBUF staging buffers
+  static constexpr int kOffBias = kOffC + kEpiWarps * NBUF * kEpiBufBytes;  // per warp: kWarpCols bf16
   // LN mode: this CTA's column half of gamma / beta (fp32), per-warp row partials and the partner's
   static constexpr int kOffGamma = kOffBias + kEpiWarps * kWarpCols * 2;
   static constexpr int kOffBeta = kOffGamma + (LN ? BN * 4 : 0);
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
                         const float* __restrict__ ln_beta, float ln_eps, int32_t M, int32_t N, int32_t K,
                         int32_t act) {
-  using S = GemmSmem<BN, STAGES, CL, LN>;
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL || LN) ? 2 : 1>;
   static_assert(!LN || (CL == 4 && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs with a residual");
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ew = warp - 2;
     const int hf = static_cast<int>(ew) / 4;
     const int row = static_cast<int>(q) * 32 + static_cast<int>(lane);  // accumulator row of this thread
-    uint8_t* cbuf = smem + S::kOffC + ew * S::kBufs * kEpiBufBytes;
+    uint8_t* cbuf = smem + S::kOffC + ew * S::kNBuf * kEpiBufBytes;
     uint64_t* rbar = res_bar + ew * S::kBufs;
     __nv_bfloat16* sbias = reinterpret_cast<__nv_bfloat16*>(smem + S::kOffBias);  // [BN] this CTA's half
     float* sgamma = reinterpret_cast<float*>(smem + S::kOffGamma);
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const uint32_t ew = warp - 2;
     const int hf = static_cast<int>(ew) / 4;  // column half of the tile
-    uint8_t* cbuf = smem + S::kOffC + ew * S::kBufs * kEpiBufBytes;
+    uint8_t* cbuf = smem + S::kOffC + ew * S::kNBuf * kEpiBufBytes;
     __nv_bfloat16* sbias = reinterpret_cast<__nv_bfloat16*>(smem + S::kOffBias + ew * S::kWarpCols * 2);
     uint64_t* rbar = res_bar + ew * S::kBufs;
     const uint32_t tmem_empty_lead0 = PAIR ? mapa_shared(&tmem_empty[0], lead_rank) : 0u;
@@ -402,7 +406,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 64; ++j) v[j] = apply_act(v[j], act);
           }
-          uint8_t* buf = cbuf + c * kEpiBufBytes;
+          uint8_t* buf = cbuf + (c % S::kNBuf) * kEpiBufBytes;
+          if (S::kNBuf == 1 && c > 0) {  // the reused buffer: the previous chunk's store has read it
+            if (lane == 0) tma_store_wait_read<0>();
+            __syncwarp();
+          }
           const uint32_t sbase = smem_u32(buf);
           if (RESIDUAL) {
             mbar_wait(&rbar[c], (res_phase >> c) & 1u);
@@ -465,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false>
 cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
-  using S = GemmSmem<BN, STAGES, CL, LN>;
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL || LN) ? 2 : 1>;
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_2d_bf16(&ta, g.a, g.k, g.m, static_cast<uint64_t>(g.k) * 2, BK, BM, true) ||
       !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, CL > 1 ? BN / 2 : BN, true) ||
@@ -521,7 +529,10 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   // smem per SM: CTA pair -> 32 KB per stage (A 16 KB + half of B) -> 5 stages; 1 CTA -> 48 KB -> 3
   if (g.residual != nullptr)
     return pair ? run_gemm<256, 5, true, 2>(g, stream) : run_gemm<256, 3, true, 1>(g, stream);
-  return pair ? run_gemm<256, 5, false, 2>(g, stream) : run_gemm<256, 3, false, 1>(g, stream);
+#ifndef CORA_GEMM_STAGES
+#define CORA_GEMM_STAGES 6
+#endif
+  return pair ? run_gemm<256, CORA_GEMM_STAGES, false, 2>(g, stream) : run_gemm<256, 3, false, 1>(g, stream);
 }
 
 bool gemm_ln_supported(const GemmArgs& g) {
