@@ -47,12 +47,13 @@ def padded_flops(lengths, d, dff) -> int:
     return useful_flops([Lp] * len(lengths), d, dff)
 
 
-def kernel_work(name, T, S2, d, dff):
+def kernel_work(name, T, S2, d, dff, heads=8):
     """(bound, algorithmic amount per launch, unit) for each layer kernel."""
     if name == "qkv_gemm":
         return "tensor", 2.0 * T * d * 3 * d, "flop"
     if name == "attention":
-        return "tensor", 4.0 * d * S2, "flop"
+        # MUFU-bound (SURVEY §8(a) a3, DESIGN.md section 6): one exp2 per useful score, H * sum L^2
+        return "alu", float(heads) * S2, "exp"
     if name == "out_proj_gemm":
         return "tensor", 2.0 * T * d * d, "flop"
     if name == "ff1_gemm":
@@ -416,9 +417,10 @@ def main():
     total_flops = useful_flops(lengths, d, dff)
     value = total_flops / (ms * 1e-3) / 1e12
     T, S2 = int(loc_len.sum()), int((loc_len ** 2).sum())
+    sm_count = int(P._lib.lib().cora_device_sm_count())
     kernels = {}
     for k in KERNELS:
-        bound, work, unit = kernel_work(k, T, S2, d, dff)
+        bound, work, unit = kernel_work(k, T, S2, d, dff, H)
         dur = kern_ms[k] * 1e-3
         if k.startswith("layernorm") and fused_ln:
             # LayerNorm runs in the preceding GEMM's epilogue (cora_linear_residual_layernorm_fwd): no
@@ -430,6 +432,15 @@ def main():
             peak = peaks["bf16_tflops_sustained"]
             kernels[k] = {"ms": kern_ms[k], "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                           "frac": ach / peak}
+        elif bound == "alu":
+            # exponentials: MUFU.EX2 16 / clk / SM (B200; 2x on B300 only) x SMs x max SM clock
+            ach = work / dur / 1e9
+            peak = 16.0 * sm_count * (clocks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e9
+            tf = 4.0 * d * S2 / dur / 1e12
+            kernels[k] = {"ms": kern_ms[k], "bound": "alu", "achieved": ach, "peak": peak, "unit": "Gexp/s",
+                          "frac": ach / peak, "peak_source": "16 MUFU.EX2/clk/SM x SMs x max SM clock (DESIGN.md)",
+                          "tensor_view": {"achieved": tf, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                                          "frac": tf / peaks["bf16_tflops_sustained"]}}
         else:
             ach = work / dur / 1e9
             peak = peaks["hbm_gbs"]
@@ -445,7 +456,9 @@ def main():
         traffic = json.load(open(tp)).get(dom)
     roofline = {"kernel": dom, "bound": kernels[dom]["bound"], "achieved": kernels[dom]["achieved"],
                 "peak": kernels[dom]["peak"], "unit": kernels[dom]["unit"], "frac": kernels[dom]["frac"],
-                "traffic": traffic, "peak_source": peaks["source"] + (" sustained" if kernels[dom]["bound"] == "tensor" else "")}
+                "traffic": traffic,
+                "peak_source": kernels[dom].get("peak_source") or (
+                    peaks["source"] + (" sustained" if kernels[dom]["bound"] == "tensor" else ""))}
 
     cpu = None
     if world == 1 and not args.no_cpu:
