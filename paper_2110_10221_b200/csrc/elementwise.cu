@@ -452,6 +452,75 @@ __global__ void __launch_bounds__(256) ragged_softmax_kernel(const T* __restrict
   }
 }
 
+// bf16 rows (L <= 512), vectorised: the row's 16-B-aligned interior is read and written as 8-element
+// vectors (<= 2 per lane), the unaligned head and tail (<= 7 elements each) by single lanes -- rows start
+// at arbitrary element offsets H*attn_off[b] + (i*H + h)*L_b.  exp2 with log2(e) folded into one FFMA.
+__global__ void __launch_bounds__(256) ragged_softmax_bf16_vec_kernel(
+    const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ lengths,
+    const int64_t* __restrict__ attn_off, const int32_t* __restrict__ seq_of_tok,
+    const int32_t* __restrict__ pos_in_seq, int32_t heads, int64_t n_rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_rows) return;
+  const int32_t t = static_cast<int32_t>(r / heads), h = static_cast<int32_t>(r % heads);
+  const int32_t b = seq_of_tok[t];
+  if (b < 0) return;  // layout status != 0
+  const int32_t i = pos_in_seq[t];
+  const int32_t L = lengths[b];
+  const int64_t base = heads * attn_off[b] + static_cast<int64_t>(i * heads + h) * L;
+  const int64_t a0 = (base + 7) & ~static_cast<int64_t>(7), a1 = (base + L) & ~static_cast<int64_t>(7);
+  const int nvec = a1 > a0 ? static_cast<int>((a1 - a0) >> 3) : 0;
+  const int head = nvec > 0 ? static_cast<int>(a0 - base) : L;  // scalar elements before the interior
+  const int tail = nvec > 0 ? static_cast<int>(base + L - a1) : 0;
+  constexpr float kLog2e = 1.4426950408889634f;
+  float v[2][8];
+  float sc = -INFINITY;  // this lane's scalar element (head: lanes 0..head-1, tail: lanes 8..8+tail-1;
+                         // short rows without an interior: lanes 0..L-1, L < 32 + 8)
+  int64_t sidx = -1;
+  if (nvec == 0) {
+    if (lane < L) sidx = base + lane;
+  } else if (lane < head) {
+    sidx = base + lane;
+  } else if (lane >= 8 && lane < 8 + tail) {
+    sidx = a1 + (lane - 8);
+  }
+  if (sidx >= 0) sc = __bfloat162float(x[sidx]);
+  float m = sc;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nvec) {
+      Vec<__nv_bfloat16>::load(x + a0 + 8 * vi, v[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m = fmaxf(m, v[k][e]);
+    }
+  }
+  m = warp_max(m) * kLog2e;
+  float s = 0.f;
+  if (sidx >= 0) {
+    sc = exp2f(fmaf(sc, kLog2e, -m));
+    s = sc;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if (lane + 32 * k < nvec) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[k][e] = exp2f(fmaf(v[k][e], kLog2e, -m));
+        s += v[k][e];
+      }
+    }
+  const float inv = 1.0f / warp_sum(s);
+  if (sidx >= 0) y[sidx] = __float2bfloat16_rn(sc * inv);
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if (lane + 32 * k < nvec) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[k][e] *= inv;
+      Vec<__nv_bfloat16>::store(y + a0 + 8 * (lane + 32 * k), v[k]);
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_layernorm(const void* x, const void* residual, const float* gamma, const float* beta, void* y,
@@ -467,6 +536,15 @@ cudaError_t launch_ragged_softmax(const cora_layout_t& L, const void* x, void* y
   const int64_t n_rows = static_cast<int64_t>(L.total_tokens) * L.heads;
   if (n_rows == 0) return cudaSuccess;
   const dim3 block(256), grid(static_cast<unsigned>((n_rows + 7) / 8));
+  // vectorised bf16 path: rows of <= 512 keys (two 8-element vectors per lane + head / tail scalars);
+  // x and y 16-B aligned so the interior vectors are aligned
+  if (dt == CORA_DT_BF16 && L.max_len <= 512 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+    ragged_softmax_bf16_vec_kernel<<<grid, block, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), L.lengths, L.attn_off, L.seq_of_tok,
+        L.pos_in_seq, L.heads, n_rows);
+    return cudaGetLastError();
+  }
   if (dt == CORA_DT_BF16)
     ragged_softmax_kernel<__nv_bfloat16, 16><<<grid, block, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), L.lengths, L.attn_off, L.seq_of_tok,

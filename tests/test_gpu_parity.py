@@ -143,6 +143,18 @@ def test_ragged_softmax_bf16_c2():
     assert rel_err(to_np(y), oracle.ragged_softmax(x, lengths, H)) <= TOL_BF16
 
 
+@pytest.mark.parametrize("lengths,H", [(EDGE_LENGTHS + [14, 15, 16, 17, 9, 0, 2], 3),
+                                       ([1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 23, 31, 33], 1)])
+def test_ragged_softmax_bf16_vector_path(lengths, H):
+    # rows start at arbitrary element offsets: vector interior + scalar head / tail, short rows scalar only
+    d = 8 * H
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 13))
+    x = synth.round_bf16(oracle.attention_scores_ragged(qkv, lengths, H))
+    lay = _layout(lengths, H)
+    y = P().ragged_softmax(lay, bf16_cuda(x))
+    assert rel_err(to_np(y), oracle.ragged_softmax(x, lengths, H)) <= TOL_BF16
+
+
 # ---------------------------------------------------------------- a2/a4/a6/a7: tcgen05 GEMM
 GEMM_SHAPES = [
     (128, 256, 64), (300, 1536, 512), (1000, 512, 2048), (257, 2048, 512), (16, 48, 16), (16, 16, 32),
