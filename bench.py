@@ -261,14 +261,18 @@ def main():
         elif events is not None:
             for e in events:
                 e.record()
-        if world > 1:
-            allgather_ragged(y_full, y_dev, tok_begin, rank, world)
         return lay
+
+    def gather():
+        # the final all-gather of the ragged outputs: eager NCCL broadcasts, outside the graph
+        allgather_ragged(y_full, y_dev, tok_begin, rank, world)
 
     # correctness gate on the benchmarked configuration (status word)
     lay = step()
     if lay is not None:
         assert lay.status() == 0, "layout status != 0"
+    if world > 1:
+        gather()
 
     for _ in range(args.warmup):
         step()
@@ -282,7 +286,7 @@ def main():
     torch.cuda.synchronize()
     graph = graph_ev = None
     if not args.no_graph:
-        # the step as ONE CUDA graph: prelude (a1) + 7 layer kernels (+ gather), chained with programmatic
+        # the step as ONE CUDA graph: prelude (a1) + the layer kernels, chained with programmatic
         # dependent launch.  graph_ev is the same step with event-record nodes between the kernels (for
         # the per-kernel breakdown; those nodes break the PDL overlap, so it is timed separately).
         graph = torch.cuda.CUDAGraph()
@@ -352,6 +356,35 @@ def main():
         ms = float(t.item())
     else:
         ms = ms_local
+
+    # ---------------------------------------------------------------- N > 1: the all-gather
+    # `value` is the compute makespan (max over ranks from a common barrier, the scaling
+    # target); the NCCL all-gather of the ragged outputs is timed alone (ii) and with the step (iii)
+    gather_info = None
+    if world > 1:
+        run_step = graph.replay if graph is not None else (lambda: step())
+        for _ in range(args.warmup):
+            gather()
+        torch.cuda.synchronize()
+        dist.barrier()
+        g_ms = float(np.mean(timed(gather, args.steps)))
+        dist.barrier()
+
+        def step_and_gather():
+            run_step()
+            gather()
+
+        sg_ms = float(np.mean(timed(step_and_gather, args.steps)))
+        t = torch.tensor([g_ms, sg_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        g_ms, sg_ms = (float(v) for v in t.tolist())
+        gather_info = {"allgather_ms": g_ms, "bytes_received_per_rank": int((int(lengths.sum()) - T_loc) * d * 2),
+                       "with_gather": {"ms_per_step": sg_ms,
+                                       "value": useful_flops(lengths, d, dff) / (sg_ms * 1e-3) / 1e12,
+                                       "unit": "TFLOP/s"},
+                       "note": "value / ms_per_step: compute makespan (prelude + layer per rank, max over ranks); "
+                               "the NCCL all-gather of the outputs runs after it (allgather_ms alone, with_gather "
+                               "end to end)"}
 
     # ---------------------------------------------------------------- the paper's 6-layer model (SURVEY f-4)
     # one layout (prelude) per batch shared by 6 layers, one CUDA graph per
@@ -486,7 +519,7 @@ def main():
                    "d_ff": dff, "parallelism": f"seq-shard{world}" if world > 1 else "single",
                    "l2": "no flush" if args.no_flush else "flushed (256 MB write) between steps",
                    "step": f"prelude(a1) + {layer_launches} layer kernels (a2..a8"
-                   + (", LayerNorm fused into the out-proj / FF2 GEMM epilogues)" if fused_ln else ")") + (" + NCCL all-gather" if world > 1 else ""),
+                   + (", LayerNorm fused into the out-proj / FF2 GEMM epilogues)" if fused_ln else ")") + (" per rank; NCCL all-gather timed separately (multi_gpu)" if world > 1 else ""),
                    "launch": "eager" if args.no_graph else "CUDA graph replay per step, programmatic dependent launch"},
         "frac_of_peak": {"burst": value / peaks["bf16_tflops"], "sustained": value / peaks["bf16_tflops_sustained"],
                          "source": peaks["source"]},
@@ -495,6 +528,7 @@ def main():
         "kernels": kernels,
         "prelude_ms": prelude_ms,
         "stack6": stack,
+        "multi_gpu": gather_info,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": (1 + layer_launches) * args.steps,
