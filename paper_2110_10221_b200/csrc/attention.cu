@@ -545,7 +545,6 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
   if (L.total_tokens == 0 || L.batch == 0) return cudaSuccess;
   const int32_t d = L.heads * head_dim;
   if (head_dim == HD) {
-    if (static_cast<int64_t>(L.total_tokens) * 3 * d >= (int64_t{1} << 31)) return cudaErrorInvalidValue;  // int32 offsets
     CUtensorMap tm;
     if (!make_tmap_2d_bf16(&tm, qkv, 3ull * d, L.total_tokens, 3ull * d * 2, HD, TQ, true))
       return cudaErrorInvalidValue;
