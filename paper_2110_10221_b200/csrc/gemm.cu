@@ -84,14 +84,16 @@ __device__ __forceinline__ float apply_act(float x, int act) {
 // (cta_group::2), pair rank r owning rows [128 r, 128 r + 128) of it; 4 (LN only) = two CTA pairs compute
 // the two BN-column halves of the same 256 rows (N = 2 BN), so every row of the output lives in one
 // cluster and its LayerNorm statistics are combined across the pairs (section "LN epilogue" below).
-template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN>
+template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN, bool LNREG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                         const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_r,
                         const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
                         const float* __restrict__ ln_beta, float ln_eps, const __nv_bfloat16* __restrict__ res_ptr,
                         int32_t M, int32_t N, int32_t K, int32_t act) {
-  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LN) ? 2 : 1>;
+  // staging buffers per epilogue warp: the residual is TMA-prefetched into one per chunk (RESIDUAL,
+  // staged LN), or the row segment lives in registers (LNREG) / there is no residual: one reused buffer
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : 1>;
   static_assert(!LN || (CL == 4 && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs with a residual");
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) acc = 0, acc_phase ^= 1;
       }
     }
-  } else if (LN) {
+  } else if (LN && LNREG) {
     // ------------------------------------------------------------ LN epilogue (every CTA)
     // Warp (q, hf) owns rows [32 q, 32 q + 32) x columns [hf 128, hf 128 + 128) of this CTA's BN-column
     // half; one thread = one row segment of 128 columns, held in REGISTERS (64 bf16 pairs) from the
@@ -344,6 +346,132 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(&tm_c, cbuf, nw + c * BK, row0);
+          tma_store_commit();
+        }
+      }
+      if (++acc == 2) acc = 0, acc_phase ^= 1;
+    }
+    if (lane == 0) tma_store_wait_all<0>();
+    __syncwarp();
+  } else if (LN) {
+    // ------------------------------------------------------------ LN epilogue, staged residual (every CTA)
+    // Warp (q, hf) owns rows [32 q, 32 q + 32) x columns [hf 128, hf 128 + 128) of this CTA's BN-column
+    // half.  pass 1: v = bf16(acc + bias + residual) into the staging buffers (the rounding point of
+    // the unfused path, Y1 / Y2) and per-row (sum v, sum v^2); the two column quarters of a row are
+    // combined in smem, the CTA partial is sent with st.async to the CTA holding the row's other
+    // column half (rank ^ 2), whose bytes complete this CTA's xch_bar; pass 2: normalise
+    // (v - mean) * rstd * gamma + beta (reading c2/c3: post-LN, biased variance) in place, TMA store.
+    const uint32_t q = warp & 3;
+    const uint32_t ew = warp - 2;
+    const int hf = static_cast<int>(ew) / 4;
+    const int row = static_cast<int>(q) * 32 + static_cast<int>(lane);  // accumulator row of this thread
+    uint8_t* cbuf = smem + S::kOffC + ew * S::kNBuf * kEpiBufBytes;
+    uint64_t* rbar = res_bar + ew * S::kBufs;
+    __nv_bfloat16* sbias = reinterpret_cast<__nv_bfloat16*>(smem + S::kOffBias);  // [BN] this CTA's half
+    float* sgamma = reinterpret_cast<float*>(smem + S::kOffGamma);
+    float* sbeta = reinterpret_cast<float*>(smem + S::kOffBeta);
+    float2* part = reinterpret_cast<float2*>(smem + S::kOffPart);  // [acc][hf][row]
+    float2* recv = reinterpret_cast<float2*>(smem + S::kOffRecv);  // [acc][row]
+    const uint32_t tmem_empty_lead0 = mapa_shared(&tmem_empty[0], lead_rank);
+    const uint32_t partner = rank ^ 2u;
+    const uint32_t recv_remote0 = mapa_shared(recv, partner);
+    const uint32_t xch_remote0 = mapa_shared(&xch_bar[0], partner);
+    const int n_half0 = half * BN;
+    // this CTA's column half of bias / gamma / beta, once
+    for (int c = static_cast<int>(threadIdx.x) - 64; c < BN; c += 32 * kEpiWarps) {
+      sbias[c] = bias != nullptr ? bias[n_half0 + c] : __float2bfloat16_rn(0.f);
+      sgamma[c] = ln_gamma[n_half0 + c];
+      sbeta[c] = ln_beta[n_half0 + c];
+    }
+    named_bar_sync(1, 32 * kEpiWarps);
+    const float inv_n = 1.0f / static_cast<float>(N);
+    int acc = 0;
+    uint32_t acc_phase = 0, res_phase = 0;
+    for (int u = unit0; u < num_units; u += unit_step) {
+      const int m0 = unit_m0(u);
+      const int nw = n_half0 + hf * S::kWarpCols;
+      const int row0 = m0 + static_cast<int>(q) * 32;
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) {
+        for (int c = 0; c < S::kBufs; ++c) {
+          mbar_arrive_expect_tx(&rbar[c], kEpiBufBytes);
+          tma_load_2d(cbuf + c * kEpiBufBytes, &tm_r, &rbar[c], nw + c * BK, row0);
+        }
+        if (ew == 0) mbar_arrive_expect_tx(&xch_bar[acc], BM * 8);  // the partner's 128 row partials
+      }
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < S::kBufs; ++c) {
+        uint32_t r[64];
+        const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN + hf * S::kWarpCols + c * BK;
+        CORA_TMEM_LD_32X32B_X32(taddr, r);
+        CORA_TMEM_LD_32X32B_X32(taddr + 32, (r + 32));
+        tmem_ld_wait();
+        if (c == S::kBufs - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_lead0 + acc * 8);
+        }
+        const uint32_t sbase = smem_u32(cbuf + c * kEpiBufBytes);
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(sbias + hf * S::kWarpCols + c * BK);
+        mbar_wait(&rbar[c], (res_phase >> c) & 1u);
+        res_phase ^= 1u << c;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t w[4];
+          ld_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
+          uint32_t o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t b2 = bw[ch * 4 + i];
+            float v0 = __uint_as_float(r[ch * 8 + 2 * i]) + bf16_lo(b2);
+            float v1 = __uint_as_float(r[ch * 8 + 2 * i + 1]) + bf16_hi(b2);
+            if (act != CORA_ACT_NONE) v0 = apply_act(v0, act), v1 = apply_act(v1, act);
+            o[i] = pack_bf16x2(v0 + bf16_lo(w[i]), v1 + bf16_hi(w[i]));
+            const float y0 = bf16_lo(o[i]), y1 = bf16_hi(o[i]);  // statistics of the rounded values
+            s1 += y0 + y1;
+            s2 = fmaf(y0, y0, fmaf(y1, y1, s2));
+          }
+          st_shared_v4(sbase + sw128_offset(lane, ch), o[0], o[1], o[2], o[3]);
+        }
+      }
+      float2* pa = part + acc * 2 * BM;
+      pa[hf * BM + row] = make_float2(s1, s2);
+      named_bar_sync(1, 32 * kEpiWarps);  // both column quarters of every row are in `part`
+      const float2 p0 = pa[row], p1 = pa[BM + row];
+      const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial
+      if (hf == 0)
+        st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
+      mbar_wait(&xch_bar[acc], acc_phase);
+      const float2 pr = recv[acc * BM + row];
+      const float mean = (c1 + pr.x) * inv_n;
+      const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
+      const float rstd = rsqrtf(var + ln_eps);
+#pragma unroll 1
+      for (int c = 0; c < S::kBufs; ++c) {
+        uint8_t* buf = cbuf + c * kEpiBufBytes;
+        const uint32_t sbase = smem_u32(buf);
+        const float* gm = sgamma + hf * S::kWarpCols + c * BK;
+        const float* bt = sbeta + hf * S::kWarpCols + c * BK;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t w[4];
+          ld_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int col = ch * 8 + 2 * i;
+            w[i] = pack_bf16x2((bf16_lo(w[i]) - mean) * rstd * gm[col] + bt[col],
+                               (bf16_hi(w[i]) - mean) * rstd * gm[col + 1] + bt[col + 1]);
+          }
+          st_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tm_c, buf, nw + c * BK, row0);
           tma_store_commit();
         }
       }
@@ -471,9 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false>
+template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false, bool LNREG = false>
 cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
-  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LN) ? 2 : 1>;
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : 1>;
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_2d_bf16(&ta, g.a, g.k, g.m, static_cast<uint64_t>(g.k) * 2, BK, BM, true) ||
       !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, CL > 1 ? BN / 2 : BN, true) ||
@@ -485,7 +613,7 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   } else {
     tr = tc;  // unused
   }
-  auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL, LN>;
+  auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL, LN, LNREG>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kAlloc);
@@ -544,10 +672,11 @@ bool gemm_ln_supported(const GemmArgs& g) {
 cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream) {
   if (g.m == 0) return cudaSuccess;
   if (!gemm_ln_supported(g)) return cudaErrorInvalidValue;
-#ifndef CORA_LN_STAGES
-#define CORA_LN_STAGES 5
-#endif
-  return run_gemm<256, CORA_LN_STAGES, true, 4, true>(g, stream);  // 2 CTA pairs per cluster
+  // 2 CTA pairs per cluster.  Long K (FF2): row segments in registers, one staging buffer, 5 stages --
+  // the mainloop is bound by the bytes in flight.  Short K (out-proj): the epilogue is the critical path,
+  // so the residual is TMA-prefetched into two staging buffers per warp (4 stages fit beside them).
+  if (g.k >= 1024) return run_gemm<256, 5, true, 4, true, true>(g, stream);
+  return run_gemm<256, 4, true, 4, true, false>(g, stream);
 }
 
 }  // namespace cora
