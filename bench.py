@@ -251,9 +251,16 @@ def main():
 
     lay_holder = {}
 
+    fwd = P.EncoderForward(params)
+
     def step(events=None, pre_event=None):
         if pre_event is not None:
             pre_event.record()
+        if events is None and len(loc_len) and T_loc:
+            # the timed step: prelude + layer in one call (cora_encoder_forward: QKV runs under the prelude)
+            fwd(len_dev, T_loc, x_dev, out=y_dev)
+            return fwd
+        # the instrumented step: separate calls, events between the kernels
         lay = P.layout_build(len_dev, T_loc, H, 512) if len(loc_len) else None
         lay_holder["lay"] = lay
         if lay is not None and T_loc:

@@ -174,6 +174,20 @@ int32_t cora_encoder_layer_launches(const cora_encoder_params_t* p, int32_t tota
 cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
                                         void* y, void* ws, size_t ws_bytes, void* stream, void* const* events);
 
+/* Workspace for cora_encoder_forward: the layout tables + the layer workspace. */
+size_t cora_encoder_forward_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
+                                            int32_t max_len);
+
+/* One ragged batch through one layer from its lengths: cora_layout_build (step a1) + the layer (a2..a8)
+ * in one call, with the tables in `ws`.  Because x must be complete before this call, the QKV GEMM does
+ * not wait for the prelude (which it does not read): it runs under it and only waits for it before
+ * completing, taking the prelude off the critical path.  lengths: device int32 [batch]; x, y as for
+ * cora_encoder_layer_fwd; layout_out (may be NULL) receives the layout (for cora_layout_status).
+ * Errors as cora_layout_build and cora_encoder_layer_fwd. */
+cora_status_t cora_encoder_forward(const cora_encoder_params_t* p, const int32_t* lengths, int32_t batch,
+                                   int32_t total_tokens, int32_t max_len, const void* x, void* y, void* ws,
+                                   size_t ws_bytes, cora_layout_t* layout_out, void* stream);
+
 /* Workspace for cora_encoder_stack_fwd: the largest layer workspace + one [T, d_model] bf16 buffer
  * (n_layers > 1); 0 on invalid arguments. */
 size_t cora_encoder_stack_workspace_bytes(const cora_encoder_params_t* layers, int32_t n_layers, int32_t total_tokens);

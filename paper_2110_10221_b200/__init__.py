@@ -7,6 +7,7 @@ it is missing -- there is no CPU or eager fallback.
 from . import _lib
 from .api import (  # noqa: F401
     EncoderLayer,
+    EncoderForward,
     EncoderParams,
     EncoderStack,
     HostForward,

@@ -22,7 +22,7 @@ LAYER_EVENTS = 8
 # Every symbol include/cora.h declares (checked by tests/test_boundary.py on CPU).
 EXPORTS = (
     "cora_layout_workspace_bytes", "cora_layout_build", "cora_layout_status", "cora_encoder_workspace_bytes",
-    "cora_encoder_layer_fwd", "cora_encoder_layer_fwd_ex", "cora_encoder_layer_launches", "cora_encoder_stack_workspace_bytes", "cora_encoder_stack_fwd", "cora_forward_host_workspace_bytes",
+    "cora_encoder_layer_fwd", "cora_encoder_layer_fwd_ex", "cora_encoder_layer_launches", "cora_encoder_stack_workspace_bytes", "cora_encoder_stack_fwd", "cora_encoder_forward_workspace_bytes", "cora_encoder_forward", "cora_forward_host_workspace_bytes",
     "cora_encoder_forward_host", "cora_linear_fwd", "cora_linear_residual_layernorm_fwd", "cora_vgemm_workspace_bytes", "cora_vgemm_fwd", "cora_trmm_fwd", "cora_ragged_attention_fwd", "cora_ragged_masked_attention_fwd", "cora_ragged_softmax_fwd",
     "cora_layernorm_fwd", "cora_shard_plan", "cora_status_string", "cora_device_sm_count", "cora_build_info",
 )
@@ -84,6 +84,9 @@ def lib() -> ctypes.CDLL:
             "cora_encoder_layer_fwd_ex": (i32, [ctypes.POINTER(EncoderParams), ctypes.POINTER(Layout), vp, vp, vp, sz, vp,
                                                 ctypes.POINTER(ctypes.c_void_p)]),
             "cora_encoder_layer_launches": (i32, [ctypes.POINTER(EncoderParams), i32]),
+            "cora_encoder_forward_workspace_bytes": (sz, [ctypes.POINTER(EncoderParams), i32, i32, i32]),
+            "cora_encoder_forward": (i32, [ctypes.POINTER(EncoderParams), vp, i32, i32, i32, vp, vp, vp, sz,
+                                           ctypes.POINTER(Layout), vp]),
             "cora_encoder_stack_workspace_bytes": (sz, [ctypes.POINTER(EncoderParams), i32, i32]),
             "cora_encoder_stack_fwd": (i32, [ctypes.POINTER(EncoderParams), i32, ctypes.POINTER(Layout), vp, vp, vp, sz,
                                              vp]),

@@ -175,6 +175,40 @@ class EncoderLayer:
         return y
 
 
+class EncoderForward:
+    """Lengths in, layer out (cora_encoder_forward): the prelude and the layer in one call; the QKV GEMM
+    runs under the prelude.  `layout` (after a call) is the batch's layout, for status()."""
+
+    def __init__(self, params: EncoderParams, max_len: int = 512):
+        self.params = params
+        self.cp = params.cstruct()
+        self.max_len = int(max_len)
+        self.ws = None
+        self.layout = C.Layout()
+
+    def __call__(self, lengths: torch.Tensor, total_tokens: int, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+        _need_cuda(lengths, x, out)
+        if lengths.dtype != torch.int32:
+            raise ValueError("lengths must be int32")
+        T, B = int(total_tokens), lengths.numel()
+        if x.dtype != torch.bfloat16 or x.shape != (T, self.params.d_model):
+            raise ValueError("x must be bf16 [T, d_model]")
+        nbytes = int(C.lib().cora_encoder_forward_workspace_bytes(ctypes.byref(self.cp), B, T, self.max_len))
+        if nbytes == 0:
+            raise C.CoraError(C.CORA_ERR_INVALID, "cora_encoder_forward_workspace_bytes")
+        if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
+            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+        y = torch.empty_like(x) if out is None else out
+        C.check(C.lib().cora_encoder_forward(ctypes.byref(self.cp), _ptr(lengths), B, T, self.max_len, _ptr(x), _ptr(y),
+                                             _ptr(self.ws), self.ws.numel(), ctypes.byref(self.layout),
+                                             _stream(stream)), "cora_encoder_forward")
+        return y
+
+    def status(self, stream=None) -> int:
+        return C.lib().cora_layout_status(ctypes.byref(self.layout), _stream(stream))
+
+
 class EncoderStack:
     """n encoder layers over one ragged batch sharing ONE layout (cora_encoder_stack_fwd): the prelude
     runs once per batch, the layers ping-pong between the output and a workspace buffer."""

@@ -309,8 +309,12 @@ cora_status_t cora_layernorm_fwd(const void* x, const void* residual, const floa
   return cuda_status(launch_layernorm(x, residual, gamma, beta, y, rows, cols, eps, dt, as_stream(stream)));
 }
 
-cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
-                                        void* y, void* ws, size_t ws_bytes, void* stream, void* const* events) {
+namespace {
+// qkv_late_wait: x was complete before the previous launch on the stream (the prelude of
+// cora_encoder_forward), so the QKV GEMM need not wait for that launch before reading x -- it runs under
+// the prelude and waits for it only before completing
+cora_status_t encoder_layer_impl(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x, void* y,
+                                 void* ws, size_t ws_bytes, void* stream, void* const* events, bool qkv_late_wait) {
   if (p == nullptr || layout == nullptr) return CORA_ERR_INVALID;
   const int32_t d = p->d_model, H = p->heads, ff = p->d_ff, T = layout->total_tokens;
   if (d <= 0 || H <= 0 || ff <= 0 || (d % H) != 0 || (d % 8) != 0 || (ff % 8) != 0 || H != layout->heads)
@@ -347,8 +351,9 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   cudaError_t e;
   // a2: QKV = x W_qkv^T + b_qkv
   mark(0);
-  if ((e = launch_gemm(GemmArgs{x, p->w_qkv, p->b_qkv, nullptr, qkv, T, 3 * d, d, CORA_ACT_NONE}, s)) != cudaSuccess)
-    return cuda_status(e);
+  GemmArgs g2{x, p->w_qkv, p->b_qkv, nullptr, qkv, T, 3 * d, d, CORA_ACT_NONE};
+  g2.late_wait = qkv_late_wait && events == nullptr;
+  if ((e = launch_gemm(g2, s)) != cudaSuccess) return cuda_status(e);
   // a3: fused ragged attention
   mark(1);
   if ((e = launch_attention(*layout, qkv, o, hd, 1.0f / sqrtf(static_cast<float>(hd)), s)) != cudaSuccess)
@@ -395,6 +400,35 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   }
   mark(7);
   return CORA_OK;
+}
+}  // namespace
+
+cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x,
+                                        void* y, void* ws, size_t ws_bytes, void* stream, void* const* events) {
+  return encoder_layer_impl(p, layout, x, y, ws, ws_bytes, stream, events, false);
+}
+
+size_t cora_encoder_forward_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
+                                            int32_t max_len) {
+  if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return 0;
+  return align_up(cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len)) +
+         carve_encoder(p, total_tokens).total;
+}
+
+cora_status_t cora_encoder_forward(const cora_encoder_params_t* p, const int32_t* lengths, int32_t batch,
+                                   int32_t total_tokens, int32_t max_len, const void* x, void* y, void* ws,
+                                   size_t ws_bytes, cora_layout_t* layout_out, void* stream) {
+  if (p == nullptr || ws == nullptr || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0) return CORA_ERR_INVALID;
+  const size_t need = cora_encoder_forward_workspace_bytes(p, batch, total_tokens, max_len);
+  if (need == 0 || ws_bytes < need) return CORA_ERR_INVALID;
+  const size_t lay_bytes = cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  cora_layout_t L;
+  cora_status_t st = cora_layout_build(lengths, batch, total_tokens, p->heads, max_len, w, lay_bytes, &L, stream);
+  if (st != CORA_OK) return st;
+  if (layout_out != nullptr) *layout_out = L;
+  const size_t off = align_up(lay_bytes);
+  return encoder_layer_impl(p, &L, x, y, w + off, ws_bytes - off, stream, nullptr, true);
 }
 
 int32_t cora_encoder_layer_launches(const cora_encoder_params_t* p, int32_t total_tokens) {
@@ -561,7 +595,7 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
     if (K == 1) {
       if (xbytes > 0 && cudaMemcpyAsync(d_x, x_host, xbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return CORA_ERR_CUDA;
-      const cora_status_t st2 = cora_encoder_layer_fwd_ex(p, &L, d_x, d_y, w, layer_ws, stream, nullptr);
+      const cora_status_t st2 = encoder_layer_impl(p, &L, d_x, d_y, w, layer_ws, stream, nullptr, true);
       if (st2 != CORA_OK) return st2;
       if (xbytes > 0 && cudaMemcpyAsync(y_host, d_y, xbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
         return CORA_ERR_CUDA;
@@ -588,8 +622,8 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
       cora_status_t st = cora_layout_build(d_len + seq_begin[c], nb, nt, p->heads, max_len, chunk_lay_ws, lay_bytes,
                                            &Lc, stream);
       if (st != CORA_OK) return st;
-      st = cora_encoder_layer_fwd_ex(p, &Lc, d_x + row * tok_begin[c], d_y + row * tok_begin[c], w, layer_ws, stream,
-                                     nullptr);
+      st = encoder_layer_impl(p, &Lc, d_x + row * tok_begin[c], d_y + row * tok_begin[c], w, layer_ws, stream, nullptr,
+                              true);
       if (st != CORA_OK) return st;
     }
     if (cudaEventRecord(hp->comp_ev[c], s) != cudaSuccess) return CORA_ERR_CUDA;

@@ -27,6 +27,7 @@ struct GemmArgs {
   const float* ln_gamma = nullptr;  // launch_gemm_ln: c = LN(act(a b^T + bias) + residual; gamma, beta, eps)
   const float* ln_beta = nullptr;
   float ln_eps = 0.f;
+  bool late_wait = false;  // a / residual complete before the previous launch: wait for it only at the end
 };
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
 bool gemm_ln_supported(const GemmArgs& g);

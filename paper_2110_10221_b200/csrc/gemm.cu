@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_r,
                         const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
                         const float* __restrict__ ln_beta, float ln_eps, const __nv_bfloat16* __restrict__ res_ptr,
-                        int32_t M, int32_t N, int32_t K, int32_t act) {
+                        int32_t M, int32_t N, int32_t K, int32_t act, int32_t late_wait) {
   // staging buffers per epilogue warp: the residual is TMA-prefetched into one per chunk (RESIDUAL,
   // staged LN), or the row segment lives in registers (LNREG) / there is no residual: one reused buffer
   using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : 1>;
@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr;
-  pdl_wait();  // the previous kernel's outputs (our A / residual) are complete and visible
+  // late_wait: the operands were complete before the previous kernel (the prelude) started, so wait for
+  // that kernel only at the end -- this grid then still completes after it (its dependents see both)
+  if (!late_wait) pdl_wait();  // the previous kernel's outputs (our A / residual) are complete and visible
   pdl_trigger();
 
   if (warp == 0) {
@@ -586,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
 
+  if (late_wait) pdl_wait();
   tc_fence_before();
   if (PAIR)
     cluster_sync_all();  // the peers may still complete_tx / arrive on this CTA's barriers until here
@@ -647,7 +650,7 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   const int grid = (units < max_clusters ? units : max_clusters) * CL;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), S::kAlloc, stream, CL, ta, tb, tc, tr,
                     static_cast<const __nv_bfloat16*>(g.bias), g.ln_gamma, g.ln_beta, g.ln_eps,
-                    static_cast<const __nv_bfloat16*>(g.residual), g.m, g.n, g.k, g.act);
+                    static_cast<const __nv_bfloat16*>(g.residual), g.m, g.n, g.k, g.act, g.late_wait ? 1 : 0);
 }
 
 }  // namespace

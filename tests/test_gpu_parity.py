@@ -415,3 +415,21 @@ def test_forward_host_matches_device_path(lengths):
     b = int(np.argmax(lengths))
     assert rel_err(y_h[ro[b]:ro[b + 1]].double().numpy(),
                    oracle.encoder_layer(x[ro[b]:ro[b + 1]], [lengths[b]], w)) <= TOL_BF16
+
+
+# ---------------------------------------------------------------- prelude + layer in one call
+@pytest.mark.parametrize("lengths", [[3, 130, 1, 64], list(synth.config("C3")[0])], ids=lambda l: f"B{len(l)}")
+def test_encoder_forward_equals_layout_plus_layer(lengths):
+    d, H, dff = 512, 8, 2048
+    w = synth.encoder_weights(d, H, dff)
+    T = int(np.sum(lengths))
+    x = bf16_cuda(synth.activations(T, d))
+    params = P().EncoderParams.from_host(w)
+    ref = P().encoder_layer(x, _layout(lengths, H), params)
+    fwd = P().EncoderForward(params)
+    Lt = torch.tensor(np.asarray(lengths, np.int32), device="cuda")
+    for _ in range(2):  # the QKV GEMM overlaps the prelude; the result must not depend on it
+        y = fwd(Lt, T, x)
+        torch.cuda.synchronize()
+        assert fwd.status() == 0
+        assert torch.equal(y, ref)
