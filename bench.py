@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-stack", action="store_true", help="skip the 6-layer stack measurement")
+    ap.add_argument("--gather", default="torch", choices=["torch", "cora"],
+                    help="N > 1 all-gather: torch.distributed broadcasts, or the library's cora_allgather_ragged")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     args = ap.parse_args()
@@ -270,9 +272,22 @@ def main():
                 e.record()
         return lay
 
+    lib_comm = None
+    if world > 1 and args.gather == "cora":
+        from paper_2110_10221_b200.dist import NcclComm
+        lib_comm = NcclComm(rank, world)
+    row_off_all = [0]
+    for L_ in lengths:
+        row_off_all.append(row_off_all[-1] + int(L_))
+
     def gather():
         # the final all-gather of the ragged outputs: eager NCCL broadcasts, outside the graph
-        allgather_ragged(y_full, y_dev, tok_begin, rank, world)
+        if lib_comm is not None:
+            if tok_begin[rank + 1] > tok_begin[rank]:
+                y_full[tok_begin[rank]:tok_begin[rank + 1]].copy_(y_dev)
+            lib_comm.allgather_ragged(y_full, row_off_all, plan)
+        else:
+            allgather_ragged(y_full, y_dev, tok_begin, rank, world)
 
     # correctness gate on the benchmarked configuration (status word)
     lay = step()

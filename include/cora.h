@@ -298,6 +298,25 @@ cora_status_t cora_trmm_fwd(const void* l, const void* b, void* c, int32_t n, in
 cora_status_t cora_shard_plan(const int32_t* lengths_host, int32_t batch, int32_t d_model, int32_t d_ff,
                               int32_t n_ranks, int32_t* seq_begin_host);
 
+/* The final all-gather of the sequence-sharded layer's ragged outputs over NCCL, resolved
+ * at run time (dlopen of libnccl.so.2: the copy torch loaded when called from Python).  Bootstrap: rank 0
+ * calls cora_comm_get_unique_id, the caller distributes the cora_comm_unique_id_bytes() bytes (e.g. with
+ * torch.distributed), every rank calls cora_comm_init (collective: all ranks, on their own GPU).
+ * CORA_ERR_NCCL if NCCL cannot be loaded or fails; CORA_ERR_INVALID on bad arguments. */
+int32_t cora_comm_unique_id_bytes(void);
+cora_status_t cora_comm_get_unique_id(void* id_out_host);
+cora_status_t cora_comm_init(void** comm, const void* nccl_unique_id_host, int32_t n_ranks, int32_t rank);
+cora_status_t cora_comm_destroy(void* comm);
+
+/* In-place variable-size all-gather of out[T, d] (dt = bf16 or fp32, device): rank r owns the rows of
+ * sequences [seq_begin_host[r], seq_begin_host[r+1]) (cora_shard_plan), i.e. rows
+ * [row_off_host[seq_begin_host[r]], row_off_host[seq_begin_host[r+1]]) (row_off_host: the batch's exclusive
+ * token prefix, host, [batch + 1]); after the call every rank holds all T rows in the original order.
+ * ncclGroupStart; one ncclBroadcast per rank with a non-empty range (root r); ncclGroupEnd -- enqueued on
+ * `stream`.  Collective: every rank of the communicator calls it with the same tables. */
+cora_status_t cora_allgather_ragged(void* comm, const int32_t* row_off_host, const int32_t* seq_begin_host,
+                                    void* out, int32_t d, cora_dtype_t dt, void* stream);
+
 /* ---------------------------------------------------------------- misc */
 const char* cora_status_string(cora_status_t s);
 /* Number of SMs of the current device (for callers sizing their own grids); -1 on error. */

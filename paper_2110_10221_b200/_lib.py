@@ -24,7 +24,7 @@ EXPORTS = (
     "cora_layout_workspace_bytes", "cora_layout_build", "cora_layout_status", "cora_encoder_workspace_bytes",
     "cora_encoder_layer_fwd", "cora_encoder_layer_fwd_ex", "cora_encoder_layer_launches", "cora_encoder_stack_workspace_bytes", "cora_encoder_stack_fwd", "cora_encoder_forward_workspace_bytes", "cora_encoder_forward", "cora_forward_host_workspace_bytes",
     "cora_encoder_forward_host", "cora_linear_fwd", "cora_linear_residual_layernorm_fwd", "cora_vgemm_workspace_bytes", "cora_vgemm_fwd", "cora_trmm_fwd", "cora_ragged_attention_fwd", "cora_ragged_masked_attention_fwd", "cora_ragged_softmax_fwd",
-    "cora_layernorm_fwd", "cora_shard_plan", "cora_status_string", "cora_device_sm_count", "cora_build_info",
+    "cora_layernorm_fwd", "cora_shard_plan", "cora_comm_unique_id_bytes", "cora_comm_get_unique_id", "cora_comm_init", "cora_comm_destroy", "cora_allgather_ragged", "cora_status_string", "cora_device_sm_count", "cora_build_info",
 )
 
 
@@ -103,6 +103,12 @@ def lib() -> ctypes.CDLL:
             "cora_ragged_softmax_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, vp]),
             "cora_layernorm_fwd": (i32, [vp, vp, vp, vp, vp, i32, i32, f32, i32, vp]),
             "cora_shard_plan": (i32, [ctypes.POINTER(ctypes.c_int32), i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32)]),
+            "cora_comm_unique_id_bytes": (i32, []),
+            "cora_comm_get_unique_id": (i32, [vp]),
+            "cora_comm_init": (i32, [ctypes.POINTER(ctypes.c_void_p), vp, i32, i32]),
+            "cora_comm_destroy": (i32, [vp]),
+            "cora_allgather_ragged": (i32, [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), vp, i32,
+                                            i32, vp]),
             "cora_status_string": (ctypes.c_char_p, [i32]),
             "cora_device_sm_count": (i32, []),
             "cora_build_info": (ctypes.c_char_p, []),

@@ -433,3 +433,18 @@ def test_encoder_forward_equals_layout_plus_layer(lengths):
         torch.cuda.synchronize()
         assert fwd.status() == 0
         assert torch.equal(y, ref)
+
+
+# ---------------------------------------------------------------- the library's NCCL all-gather (one rank)
+def test_library_nccl_allgather_single_rank():
+    from paper_2110_10221_b200.dist import NcclComm, shard_rows
+
+    lengths = [3, 130, 1, 64]
+    plan, tok_begin = shard_rows(lengths, 512, 2048, 1)
+    comm = NcclComm(rank=0, world=1)
+    out = torch.randn(sum(lengths), 512, device="cuda").to(torch.bfloat16)
+    ref = out.clone()
+    comm.allgather_ragged(out, oracle.row_offsets(lengths), plan)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)  # one rank owns every row: the in-place gather leaves them unchanged
+    comm.close()
