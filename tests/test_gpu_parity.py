@@ -448,3 +448,23 @@ def test_library_nccl_allgather_single_rank():
     torch.cuda.synchronize()
     assert torch.equal(out, ref)  # one rank owns every row: the in-place gather leaves them unchanged
     comm.close()
+
+
+def test_layer_nan_poisoned_workspace_and_output():
+    # every workspace byte and the output start as NaN (0xFF bytes): nothing uninitialised may leak into
+    # valid outputs (tail rows of tiles, masked keys, the LayerNorm statistics exchange)
+    lengths = [3, 130, 1, 64, 0, 257, 2]
+    d, H, dff = 512, 8, 2048
+    w = synth.encoder_weights(d, H, dff)
+    T = int(np.sum(lengths))
+    x = bf16_cuda(synth.activations(T, d))
+    params = P().EncoderParams.from_host(w)
+    lay = _layout(lengths, H)
+    ref = P().encoder_layer(x, lay, params)
+    layer = P().EncoderLayer(params)
+    layer.ws = torch.full((layer.workspace_bytes(T) + 256,), 0xFF, dtype=torch.uint8, device="cuda")
+    out = torch.full((T, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    y = layer(x, lay, out=out)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y.float()).all()
+    assert torch.equal(y, ref)
