@@ -90,10 +90,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_r,
                         const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
                         const float* __restrict__ ln_beta, float ln_eps, const __nv_bfloat16* __restrict__ res_ptr,
-                        int32_t M, int32_t N, int32_t K, int32_t act, int32_t late_wait) {
+                        __nv_bfloat16* __restrict__ out_ptr, int32_t M, int32_t N, int32_t K, int32_t act,
+                        int32_t late_wait) {
   // staging buffers per epilogue warp: the residual is TMA-prefetched into one per chunk (RESIDUAL,
   // staged LN), or the row segment lives in registers (LNREG) / there is no residual: one reused buffer
-  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : 1>;
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : (LNREG ? 0 : 1)>;
   static_assert(!LN || (CL == 4 && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs with a residual");
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -324,14 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float mean = (c1 + pr.x) * inv_n;
       const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
       const float rstd = rsqrtf(var + ln_eps);
-      const uint32_t sbase = smem_u32(cbuf);
+      // straight from registers to the row in global memory (16-B stores; no staging buffer, whose 32 KB
+      // hold a sixth pipeline stage instead)
+      uint4* dst = reinterpret_cast<uint4*>(out_ptr + static_cast<size_t>(grow) * N + nw);
 #pragma unroll
       for (int c = 0; c < kSeg / BK; ++c) {
         const float* gm = sgamma + hf * kSeg + c * BK;
         const float* bt = sbeta + hf * kSeg + c * BK;
-        // the single staging buffer: the previous store must have finished reading it
-        if (lane == 0) tma_store_wait_read<0>();
-        __syncwarp();
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
           uint32_t w[4];
@@ -342,19 +342,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             w[i2] = pack_bf16x2((bf16_lo(vw) - mean) * rstd * gm[col] + bt[col],
                                 (bf16_hi(vw) - mean) * rstd * gm[col + 1] + bt[col + 1]);
           }
-          st_shared_v4(sbase + sw128_offset(lane, ch), w[0], w[1], w[2], w[3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tm_c, cbuf, nw + c * BK, row0);
-          tma_store_commit();
+          if (grow < M) dst[c * 8 + ch] = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
+      (void)row0;
       if (++acc == 2) acc = 0, acc_phase ^= 1;
     }
-    if (lane == 0) tma_store_wait_all<0>();
-    __syncwarp();
   } else if (LN) {
     // ------------------------------------------------------------ LN epilogue, staged residual (every CTA)
     // Warp (q, hf) owns rows [32 q, 32 q + 32) x columns [hf 128, hf 128 + 128) of this CTA's BN-column
@@ -604,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false, bool LNREG = false>
 cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
-  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : 1>;
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : (LNREG ? 0 : 1)>;
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_2d_bf16(&ta, g.a, g.k, g.m, static_cast<uint64_t>(g.k) * 2, BK, BM, true) ||
       !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, CL > 1 ? BN / 2 : BN, true) ||
@@ -650,7 +643,8 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   const int grid = (units < max_clusters ? units : max_clusters) * CL;
   return launch_pdl(kern, dim3(grid), dim3(kThreads), S::kAlloc, stream, CL, ta, tb, tc, tr,
                     static_cast<const __nv_bfloat16*>(g.bias), g.ln_gamma, g.ln_beta, g.ln_eps,
-                    static_cast<const __nv_bfloat16*>(g.residual), g.m, g.n, g.k, g.act, g.late_wait ? 1 : 0);
+                    static_cast<const __nv_bfloat16*>(g.residual), static_cast<__nv_bfloat16*>(g.c), g.m, g.n, g.k,
+                    g.act, g.late_wait ? 1 : 0);
 }
 
 }  // namespace
@@ -678,7 +672,7 @@ cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream) {
   // 2 CTA pairs per cluster.  Long K (FF2): row segments in registers, one staging buffer, 5 stages --
   // the mainloop is bound by the bytes in flight.  Short K (out-proj): the epilogue is the critical path,
   // so the residual is TMA-prefetched into two staging buffers per warp (4 stages fit beside them).
-  if (g.k >= 1024) return run_gemm<256, 5, true, 4, true, true>(g, stream);
+  if (g.k >= 1024) return run_gemm<256, 6, true, 4, true, true>(g, stream);
   return run_gemm<256, 4, true, 4, true, false>(g, stream);
 }
 
