@@ -10,7 +10,8 @@
 // longest-first tile list built by the prelude (static stride over the list).  For one work
 // tile (b, h, qt): Q = 128 query rows of sequence b, head h; K_j / V_j = 128-key tiles,
 // j < ceil(L_b / 128).
-//   warp 0     : TMA producer (Q x2, K ring of 2, V ring of 2) from QKV[T, 3d], 128x64 SWIZZLE_128B boxes
+//   warp 0     : TMA producers from QKV[T, 3d], 128x64 SWIZZLE_128B boxes: lane 0 Q (2 slots) + K (3-deep
+//                ring), lane 1 V (2-deep ring)
 //   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer
 //                  S_j = Q K_j^T  (M128 N128 K64, SS form, fp32 in TMEM cols [0,128))
 //                  O  += P_j V_j  (M128 N64 K128, TS form: P read from TMEM cols [128,192) as bf16
@@ -25,8 +26,10 @@
 //                  belong to the next sequence and are never written).
 // Rows of a 128-row TMA box that lie past the sequence end are real rows of the next
 // sequence (finite) or TMA zero-fill past T: their keys are masked and their queries discarded.
-// Two CTAs per SM (96 KB smem, 256 TMEM columns each) overlap one CTA's softmax with the other's MMAs.
-// Nothing of S or P goes through shared memory or HBM.
+// Two CTAs per SM (112 KB smem, 256 TMEM columns each) overlap one CTA's softmax with the other's MMAs.
+// Nothing of S or P goes through shared memory or HBM.  Short sequences may share a tile (packed window,
+// block-diagonal mask, SURVEY f-4); causal attention (f-2) skips KV tiles above the diagonal.  The
+// softmax warps prefetch the next tile's metadata into shared memory with cp.async.
 #include <cuda_bf16.h>
 
 #include <cstdint>

@@ -19,11 +19,15 @@
 //                 place -> TMA store (32 rows x 64 cols per chunk)
 //   TMEM holds two BN-column fp32 accumulators so the epilogue of tile i overlaps the main loop of
 //   tile i+1.  A single m-block (M <= 128) runs the 1-CTA variant (cta_group::1, M=128).
+// The mainloop is bound by the bytes in flight (stages x stage bytes / TMA latency): non-residual GEMMs
+// keep one reused staging buffer per epilogue warp and 6 stages.
+// LN (N = 512, steps a4+a5 / a7+a8): two CTA pairs of one 4-CTA cluster hold the two 256-column halves
+// of the same 256 rows and combine LayerNorm row statistics over DSMEM.  Short K (out-proj, epilogue-
+// bound): residual TMA-staged, 4 stages.  Long K (FF2, mainloop-bound): LNREG -- row segments in
+// registers, rows stored straight to global memory, 6 stages.
 #include <cuda_bf16.h>
 
 #include <cstdint>
-#include <cstdio>
-#include <cstdlib>
 
 #include "cora_internal.h"
 #include "ptx.cuh"
