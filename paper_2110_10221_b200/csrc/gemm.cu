@@ -28,6 +28,8 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "cora_internal.h"
 #include "ptx.cuh"
