@@ -290,6 +290,26 @@ def test_layer_c4_sampled_sequences():
         assert rel_err(y[ro[b]:ro[b] + L], ref) <= TOL_BF16, b
 
 
+@pytest.mark.parametrize("batch,hi", [(3, 200), (12, 300), (24, 400), (40, 512)])
+def test_layer_small_t_splitk(batch, hi):
+    # small T (a few to ~20 256-row units for 33 four-CTA clusters: the fused GEMM + LN kernels run one
+    # partial wave) against the oracle, whole batch or sampled
+    lengths = synth.uniform_lengths(batch, 1, hi, seed=70 + batch)
+    d, H, dff = 512, 8, 2048
+    w = synth.encoder_weights(d, H, dff)
+    T = int(lengths.sum())
+    x = synth.activations(T, d)
+    params = P().EncoderParams.from_host(w)
+    y = to_np(P().encoder_layer(bf16_cuda(x), _layout(lengths, H), params))
+    assert P().EncoderLayer(params).launches(T) == 5
+    ro = oracle.row_offsets(lengths)
+    sample = range(len(lengths)) if T <= 3000 else [0, 1, int(np.argmax(lengths)), len(lengths) - 1]
+    for b in sample:
+        L = int(lengths[b])
+        ref = oracle.encoder_layer(x[ro[b]:ro[b] + L], [L], w)
+        assert rel_err(y[ro[b]:ro[b] + L], ref) <= TOL_BF16, b
+
+
 # ---------------------------------------------------------------- GPU self-consistency (bitwise)
 def test_layer_sequence_independence_and_permutation():
     lengths = np.array([100, 7, 300, 1, 129, 64])
