@@ -232,8 +232,10 @@ cora_status_t cora_linear_fwd(const void* a, const void* w, const void* bias, co
 /* c[m, n] = LN(act(a w^T + bias) + residual; gamma, beta, eps) with the LayerNorm (post-LN, biased
  * variance, fp32 statistics of the bf16-rounded pre-LN values, readings
  * c2/c3) fused into the GEMM epilogue: a 4-CTA cluster (two CTA pairs) owns full rows and exchanges the
- * row statistics through distributed shared memory.  Requires n == 512 and m > 128 (returns
- * CORA_ERR_UNSUPPORTED otherwise); residual, gamma, beta non-NULL; bias may be NULL. */
+ * row statistics through distributed shared memory.  The fused kernel needs n == 512, m > 128 and
+ * act == CORA_ACT_NONE; with an activation (n == 512, m > 128, or any n % 8 == 0) the call runs the
+ * GEMM into a stream-ordered temporary (cudaMallocAsync) and then the LayerNorm kernel.  Other shapes
+ * with act NONE return CORA_ERR_UNSUPPORTED; residual, gamma, beta non-NULL; bias may be NULL. */
 cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, const void* bias, const void* residual,
                                                  const float* gamma, const float* beta, float eps, void* c, int32_t m,
                                                  int32_t n, int32_t k, cora_act_t act, void* stream);

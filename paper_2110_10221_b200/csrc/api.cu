@@ -235,8 +235,17 @@ cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, c
   g.ln_gamma = gamma;
   g.ln_beta = beta;
   g.ln_eps = eps;
-  if (!gemm_ln_supported(g)) return CORA_ERR_UNSUPPORTED;
-  return cuda_status(launch_gemm_ln(g, as_stream(stream)));
+  if (gemm_ln_supported(g)) return cuda_status(launch_gemm_ln(g, as_stream(stream)));
+  if (act == CORA_ACT_NONE || (n % 8) != 0) return CORA_ERR_UNSUPPORTED;
+  // with an activation: act(a w^T + bias) + residual into a stream-ordered temporary, then LayerNorm
+  cudaStream_t s = as_stream(stream);
+  void* tmp = nullptr;
+  if (cudaMallocAsync(&tmp, static_cast<size_t>(m) * n * 2, s) != cudaSuccess) return CORA_ERR_CUDA;
+  g.c = tmp;
+  cudaError_t e = launch_gemm(g, s);
+  if (e == cudaSuccess) e = launch_layernorm(tmp, nullptr, gamma, beta, c, m, n, eps, CORA_DT_BF16, s);
+  const cudaError_t f = cudaFreeAsync(tmp, s);
+  return cuda_status(e != cudaSuccess ? e : f);
 }
 
 size_t cora_vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host) {

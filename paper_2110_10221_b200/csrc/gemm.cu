@@ -34,6 +34,23 @@
 #include "cora_internal.h"
 #include "ptx.cuh"
 
+#ifdef CORA_GEMM_TRACE
+// profiling build only: %globaltimer stamps of the phases of every CTA of the last launch
+__device__ unsigned long long g_gemm_trace[2048 * 16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GTRACE(k) (LNREG ? (void)(g_gemm_trace[blockIdx.x * 16 + (k)] = gtime()) : (void)0)  // FF2 + LN2 only
+extern "C" int cora_debug_gemm_trace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_gemm_trace, sizeof(unsigned long long) * (n < 2048 * 16 ? n : 2048 * 16)) ==
+                 cudaSuccess ? 0 : 1;
+}
+#else
+#define GTRACE(k) ((void)0)
+#endif
+
 namespace cora {
 namespace {
 
@@ -113,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* res_bar = tmem_empty + 2;  // [kEpiWarps][kBufs]
   uint64_t* xch_bar = res_bar + kEpiWarps * S::kBufs;  // [2 acc] partner's row partials landed (LN)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(xch_bar + 2);
+  if (threadIdx.x == 0) GTRACE(0);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m_blocks = (M + BM - 1) / BM;
@@ -166,7 +184,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_ptr;
   // late_wait: the operands were complete before the previous kernel (the prelude) started, so wait for
   // that kernel only at the end -- this grid then still completes after it (its dependents see both)
+  if (threadIdx.x == 0) GTRACE(1);
   if (!late_wait) pdl_wait();  // the previous kernel's outputs (our A / residual) are complete and visible
+  if (threadIdx.x == 0) GTRACE(2);
   pdl_trigger();
 
   if (warp == 0) {
@@ -209,6 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (u == unit0 && kb == 0) GTRACE(3);
+          if (u == unit0 && kb == k_blocks / 2) GTRACE(4);
+          if (u == unit0 && kb == k_blocks - 1) GTRACE(5);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + S::kOffA + stage * S::kABytes);
           const uint32_t b_addr = smem_u32(smem + S::kOffB + stage * S::kBBytes);
@@ -272,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     named_bar_sync(1, 32 * kEpiWarps);
     const float inv_n = 1.0f / static_cast<float>(N);
     constexpr int kSeg = S::kWarpCols;  // 128 columns per thread
+    const bool v8_ok = ((reinterpret_cast<uintptr_t>(res_ptr) | reinterpret_cast<uintptr_t>(out_ptr)) & 31u) == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = unit0; u < num_units; u += unit_step) {
@@ -281,15 +305,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int grow = m0 + row;  // global row of this thread
       uint32_t vv[kSeg / 2];      // the row segment as bf16 pairs: residual, then v
       {
-        const uint4* src = reinterpret_cast<const uint4*>(res_ptr + static_cast<size_t>(grow) * N + nw);
+        // 32-B loads: each lane reads whole sectors of its row (residual base 32-B aligned; else 16-B loads)
+        const __nv_bfloat16* src = res_ptr + static_cast<size_t>(grow) * N + nw;
 #pragma unroll
-        for (int g = 0; g < kSeg / 8; ++g) {
-          const uint4 w = grow < M ? __ldg(src + g) : make_uint4(0u, 0u, 0u, 0u);
-          vv[4 * g] = w.x, vv[4 * g + 1] = w.y, vv[4 * g + 2] = w.z, vv[4 * g + 3] = w.w;
+        for (int g = 0; g < kSeg / 16; ++g) {
+          uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+          if (grow < M) {
+            if (v8_ok) {
+              ld_global_nc_v8(src + g * 16, w);
+            } else {
+              const uint4 a = __ldg(reinterpret_cast<const uint4*>(src + g * 16));
+              const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + g * 16 + 8));
+              w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) vv[8 * g + e] = w[e];
         }
       }
       if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&xch_bar[acc], BM * 8);  // the partner's 128 row partials
       mbar_wait(&tmem_full[acc], acc_phase);
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
+#ifdef CORA_GEMM_TRACE
+      if (LNREG && u == unit0 && ew == 0) {  // the residual segments of every lane have arrived
+        uint32_t x = 0;
+#pragma unroll
+        for (int e = 0; e < kSeg / 2; ++e) x |= vv[e];
+        x = __reduce_or_sync(0xffffffffu, x);
+        if (lane == 0) {
+          g_gemm_trace[blockIdx.x * 16 + 10] = x;
+          GTRACE(11);
+        }
+      }
+#endif
       tc_fence_after();
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -299,18 +347,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         CORA_TMEM_LD_32X32B_X32(taddr, r);
         CORA_TMEM_LD_32X32B_X32(taddr + 32, (r + 32));
         tmem_ld_wait();
+#ifdef CORA_GEMM_TRACE
+        if (u == unit0 && ew == 0 && lane == 0) {  // the TMEM data has arrived
+          g_gemm_trace[blockIdx.x * 16 + 13 + c] = r[0] ^ r[63];
+          GTRACE(c == 0 ? 15 : 12);
+        }
+#endif
         if (c == kSeg / BK - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tmem_empty_lead0 + acc * 8);
+          if (u == unit0 && ew == 0 && lane == 0) GTRACE(14);
         }
         const uint32_t* bw = reinterpret_cast<const uint32_t*>(sbias + hf * kSeg + c * BK);
 #pragma unroll
         for (int p2 = 0; p2 < 32; ++p2) {
           const uint32_t b2 = bw[p2];
-          float v0 = __uint_as_float(r[2 * p2]) + bf16_lo(b2);
-          float v1 = __uint_as_float(r[2 * p2 + 1]) + bf16_hi(b2);
-          if (act != CORA_ACT_NONE) v0 = apply_act(v0, act), v1 = apply_act(v1, act);
+          const float v0 = __uint_as_float(r[2 * p2]) + bf16_lo(b2);
+          const float v1 = __uint_as_float(r[2 * p2 + 1]) + bf16_hi(b2);
           const uint32_t rw = vv[c * 32 + p2];
           const uint32_t o = pack_bf16x2(v0 + bf16_lo(rw), v1 + bf16_hi(rw));
           vv[c * 32 + p2] = o;
@@ -321,37 +375,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float2* pa = part + acc * 2 * BM;
       pa[hf * BM + row] = make_float2(s1, s2);
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(13);
       named_bar_sync(1, 32 * kEpiWarps);  // both column quarters of every row are in `part`
       const float2 p0 = pa[row], p1 = pa[BM + row];
       const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial
       if (hf == 0)
         st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
       mbar_wait(&xch_bar[acc], acc_phase);
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(7);
       const float2 pr = recv[acc * BM + row];
       const float mean = (c1 + pr.x) * inv_n;
       const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
       const float rstd = rsqrtf(var + ln_eps);
       // straight from registers to the row in global memory (16-B stores; no staging buffer, whose 32 KB
       // hold a sixth pipeline stage instead)
-      uint4* dst = reinterpret_cast<uint4*>(out_ptr + static_cast<size_t>(grow) * N + nw);
+      __nv_bfloat16* dst = out_ptr + static_cast<size_t>(grow) * N + nw;
 #pragma unroll
       for (int c = 0; c < kSeg / BK; ++c) {
         const float* gm = sgamma + hf * kSeg + c * BK;
         const float* bt = sbeta + hf * kSeg + c * BK;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t w[4];
+        for (int ch = 0; ch < 4; ++ch) {  // 16 columns = one 32-B sector per store
+          uint32_t w[8];
 #pragma unroll
-          for (int i2 = 0; i2 < 4; ++i2) {
-            const int col = ch * 8 + 2 * i2;
-            const uint32_t vw = vv[c * 32 + ch * 4 + i2];
+          for (int i2 = 0; i2 < 8; ++i2) {
+            const int col = ch * 16 + 2 * i2;
+            const uint32_t vw = vv[c * 32 + ch * 8 + i2];
             w[i2] = pack_bf16x2((bf16_lo(vw) - mean) * rstd * gm[col] + bt[col],
                                 (bf16_hi(vw) - mean) * rstd * gm[col + 1] + bt[col + 1]);
           }
-          if (grow < M) dst[c * 8 + ch] = make_uint4(w[0], w[1], w[2], w[3]);
+          if (grow < M) {
+            if (v8_ok) {
+              st_global_v8(dst + c * BK + ch * 16, w);
+            } else {
+              uint4* d4 = reinterpret_cast<uint4*>(dst + c * BK + ch * 16);
+              d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+          }
         }
       }
       (void)row0;
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(8);
       if (++acc == 2) acc = 0, acc_phase ^= 1;
     }
   } else if (LN) {
@@ -428,9 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint32_t b2 = bw[ch * 4 + i];
-            float v0 = __uint_as_float(r[ch * 8 + 2 * i]) + bf16_lo(b2);
-            float v1 = __uint_as_float(r[ch * 8 + 2 * i + 1]) + bf16_hi(b2);
-            if (act != CORA_ACT_NONE) v0 = apply_act(v0, act), v1 = apply_act(v1, act);
+            const float v0 = __uint_as_float(r[ch * 8 + 2 * i]) + bf16_lo(b2);
+            const float v1 = __uint_as_float(r[ch * 8 + 2 * i + 1]) + bf16_hi(b2);
             o[i] = pack_bf16x2(v0 + bf16_lo(w[i]), v1 + bf16_hi(w[i]));
             const float y0 = bf16_lo(o[i]), y1 = bf16_hi(o[i]);  // statistics of the rounded values
             s1 += y0 + y1;
@@ -588,11 +652,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   if (late_wait) pdl_wait();
+  if (threadIdx.x == 64) GTRACE(9);
   tc_fence_before();
   if (PAIR)
     cluster_sync_all();  // the peers may still complete_tx / arrive on this CTA's barriers until here
   else
     __syncthreads();
+  if (threadIdx.x == 64) GTRACE(10);
   if (warp == 1) {
     if (PAIR)
       tmem_dealloc_cg2<S::kTmemCols>(tmem_base);
@@ -668,8 +734,10 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
 }
 
 bool gemm_ln_supported(const GemmArgs& g) {
-  return g.n == 512 && g.residual != nullptr && g.ln_gamma != nullptr && g.ln_beta != nullptr &&
-         ((g.m + BM - 1) / BM) >= 2;
+  // act NONE only (the layer's a4 / a7): with the activation variants compiled in, the fully unrolled
+  // epilogue is 4x the code and a one-unit-per-CTA launch stalls on cold instruction fetches
+  return g.n == 512 && g.act == CORA_ACT_NONE && g.residual != nullptr && g.ln_gamma != nullptr &&
+         g.ln_beta != nullptr && ((g.m + BM - 1) / BM) >= 2;
 }
 
 cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream) {

@@ -199,6 +199,22 @@ def test_linear_residual_layernorm_fused(m, k, use_bias):
     assert rel_err(to_np(c), ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("act", ["relu", "gelu"])
+def test_linear_residual_layernorm_with_activation(act):
+    # activations take the two-launch path (GEMM + activation + residual, then LayerNorm)
+    m, k, n = 300, 512, 512
+    a = synth.round_bf16(synth.normal((m, k), 47))
+    w = synth.round_bf16(synth.normal((n, k), 48) / math.sqrt(k))
+    b = synth.round_bf16(synth.normal((n,), 49))
+    r = synth.round_bf16(synth.normal((m, n), 50))
+    g = synth.round_f32(1 + 0.1 * synth.normal((n,), 51))
+    be = synth.round_f32(0.1 * synth.normal((n,), 52))
+    c = P().linear_residual_layernorm(bf16_cuda(a), bf16_cuda(w), bf16_cuda(r), f32_cuda(g), f32_cuda(be),
+                                      bias=bf16_cuda(b), act=act)
+    ref = oracle.layernorm(oracle.linear(a, w, b, residual=r, act=act), g, be)
+    assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
 def test_linear_residual_layernorm_unsupported_shape():
     a = bf16_cuda(synth.normal((300, 64), 1))
     w = bf16_cuda(synth.normal((256, 64), 2))
