@@ -107,7 +107,7 @@ __device__ __forceinline__ float apply_act(float x, int act) {
 // (cta_group::2), pair rank r owning rows [128 r, 128 r + 128) of it; 4 (LN only) = two CTA pairs compute
 // the two BN-column halves of the same 256 rows (N = 2 BN), so every row of the output lives in one
 // cluster and its LayerNorm statistics are combined across the pairs (section "LN epilogue" below).
-template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN, bool LNREG>
+template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN, bool LNREG, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                         const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_r,
@@ -595,9 +595,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[2 * j] = __uint_as_float(r[2 * j]) + bf16_lo(b2);
             v[2 * j + 1] = __uint_as_float(r[2 * j + 1]) + bf16_hi(b2);
           }
-          if (act != CORA_ACT_NONE) {
+          if constexpr (ACT != CORA_ACT_NONE) {  // a compile-time variant: one epilogue body per kernel
 #pragma unroll
-            for (int j = 0; j < 64; ++j) v[j] = apply_act(v[j], act);
+            for (int j = 0; j < 64; ++j) v[j] = apply_act(v[j], ACT);
           }
           uint8_t* buf = cbuf + (c % S::kNBuf) * kEpiBufBytes;
           if (S::kNBuf == 1 && c > 0) {  // the reused buffer: the previous chunk's store has read it
@@ -667,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false, bool LNREG = false>
+template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false, bool LNREG = false, int ACT = CORA_ACT_NONE>
 cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : (LNREG ? 0 : 1)>;
   CUtensorMap ta, tb, tc, tr;
@@ -681,7 +681,7 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   } else {
     tr = tc;  // unused
   }
-  auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL, LN, LNREG>;
+  auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL, LN, LNREG, ACT>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kAlloc);
@@ -721,16 +721,34 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
 
 }  // namespace
 
+#ifndef CORA_GEMM_STAGES
+#define CORA_GEMM_STAGES 6
+#endif
+namespace {
+template <int ACT>
+cudaError_t launch_gemm_act(const GemmArgs& g, bool pair, cudaStream_t stream) {
+  if (g.residual != nullptr)
+    return pair ? run_gemm<256, 5, true, 2, false, false, ACT>(g, stream)
+                : run_gemm<256, 3, true, 1, false, false, ACT>(g, stream);
+  return pair ? run_gemm<256, CORA_GEMM_STAGES, false, 2, false, false, ACT>(g, stream)
+              : run_gemm<256, 3, false, 1, false, false, ACT>(g, stream);
+}
+}  // namespace
+
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   if (g.m == 0 || g.n == 0) return cudaSuccess;
   const bool pair = ((g.m + BM - 1) / BM) >= 2;  // a single m-block runs on one CTA
   // smem per SM: CTA pair -> 32 KB per stage (A 16 KB + half of B) -> 5 stages; 1 CTA -> 48 KB -> 3
-  if (g.residual != nullptr)
-    return pair ? run_gemm<256, 5, true, 2>(g, stream) : run_gemm<256, 3, true, 1>(g, stream);
-#ifndef CORA_GEMM_STAGES
-#define CORA_GEMM_STAGES 6
-#endif
-  return pair ? run_gemm<256, CORA_GEMM_STAGES, false, 2>(g, stream) : run_gemm<256, 3, false, 1>(g, stream);
+  switch (g.act) {
+    case CORA_ACT_NONE:
+      return launch_gemm_act<CORA_ACT_NONE>(g, pair, stream);
+    case CORA_ACT_RELU:
+      return launch_gemm_act<CORA_ACT_RELU>(g, pair, stream);
+    case CORA_ACT_GELU_ERF:
+      return launch_gemm_act<CORA_ACT_GELU_ERF>(g, pair, stream);
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 bool gemm_ln_supported(const GemmArgs& g) {
