@@ -42,7 +42,9 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define GTRACE(k) (LNREG ? (void)(g_gemm_trace[blockIdx.x * 16 + (k)] = gtime()) : (void)0)  // FF2 + LN2 only
+// CORA_GEMM_TRACE = 1: FF2 + LN2 (register LN), 2: out-proj + LN1 (staged LN), 3: plain GEMMs (last: FF1)
+#define GTRACE_ON ((CORA_GEMM_TRACE == 1 && LNREG) || (CORA_GEMM_TRACE == 2 && LN && !LNREG) || (CORA_GEMM_TRACE == 3 && !LN))
+#define GTRACE(k) (GTRACE_ON ? (void)(g_gemm_trace[blockIdx.x * 16 + (k)] = gtime()) : (void)0)
 extern "C" int cora_debug_gemm_trace(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_gemm_trace, sizeof(unsigned long long) * (n < 2048 * 16 ? n : 2048 * 16)) ==
                  cudaSuccess ? 0 : 1;
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ew == 0) mbar_arrive_expect_tx(&xch_bar[acc], BM * 8);  // the partner's 128 row partials
       }
       mbar_wait(&tmem_full[acc], acc_phase);
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       tc_fence_after();
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
@@ -511,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (hf == 0)
         st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
       mbar_wait(&xch_bar[acc], acc_phase);
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(7);
       const float2 pr = recv[acc * BM + row];
       const float mean = (c1 + pr.x) * inv_n;
       const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
@@ -540,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_store_commit();
         }
       }
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(8);
       if (++acc == 2) acc = 0, acc_phase ^= 1;
     }
     if (lane == 0) tma_store_wait_all<0>();
@@ -578,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       mbar_wait(&tmem_full[acc], acc_phase);
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < S::kBufs; ++c) {
@@ -645,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (u == unit0 && ew == 0 && lane == 0) GTRACE(8);
       if (++acc == 2) acc = 0, acc_phase ^= 1;
     }
     if (lane == 0) tma_store_wait_all<0>();
