@@ -59,17 +59,23 @@ namespace {
 constexpr int BM = 128;  // accumulator rows per CTA
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, each owning half of the tile's columns
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+#ifndef CORA_LN_EW
+#define CORA_LN_EW 16
+#endif
+// epilogue warps: 8, or 16 (four per quadrant, a quarter of the columns each) for the staged-residual LN
+// epilogue of the short-K out-projection, which is epilogue-bound
+template <bool LN, bool LNREG>
+constexpr int epi_warps() { return (LN && !LNREG) ? CORA_LN_EW : kEpiWarps; }
 constexpr int kEpiRows = 32;                      // rows per epilogue warp
 constexpr int kEpiBufBytes = kEpiRows * BK * 2;   // 4 KB staging buffer (32 rows x 128 B)
 
 // NBUF: staging buffers per epilogue warp -- one per 64-column chunk when a residual is TMA-prefetched into
 // them (RESIDUAL / LN), else one reused buffer, which frees 32 KB for a sixth pipeline stage (the mainloop
 // is bound by the bytes in flight: stages x stage bytes / TMA latency)
-template <int BN, int STAGES, int CL, bool LN, int NBUF = 2>
+template <int BN, int STAGES, int CL, bool LN, int NBUF = 2, int EW = kEpiWarps>
 struct GemmSmem {
   static constexpr int kChunks = BN / BK;             // 64-column epilogue chunks per tile
-  static constexpr int kWarpCols = BN / 2;            // columns per epilogue warp
+  static constexpr int kWarpCols = BN * 4 / EW;       // columns per epilogue warp
   static constexpr int kBufs = kWarpCols / BK;        // staging buffers per epilogue warp (one per chunk)
   static constexpr int kABytes = BM * BK * 2;         // this CTA's A rows
   static constexpr int kBBytes = (CL > 1 ? BN / 2 : BN) * BK * 2;  // this CTA's share of the B tile
@@ -78,15 +84,15 @@ struct GemmSmem {
   static constexpr int kOffB = kOffA + STAGES * kABytes;
   static constexpr int kNBuf = NBUF;
   static constexpr int kOffC = kOffB + STAGES * kBBytes;  // per warp: NBUF staging buffers
-  static constexpr int kOffBias = kOffC + kEpiWarps * NBUF * kEpiBufBytes;  // per warp: kWarpCols bf16
+  static constexpr int kOffBias = kOffC + EW * NBUF * kEpiBufBytes;  // per warp: kWarpCols bf16
   // LN mode: this CTA's column half of gamma / beta (fp32), per-warp row partials and the partner's
-  static constexpr int kOffGamma = kOffBias + kEpiWarps * kWarpCols * 2;
+  static constexpr int kOffGamma = kOffBias + EW * kWarpCols * 2;
   static constexpr int kOffBeta = kOffGamma + (LN ? BN * 4 : 0);
-  static constexpr int kOffPart = kOffBeta + (LN ? BN * 4 : 0);  // float2 [2 acc][2 halves][128 rows]
-  static constexpr int kOffRecv = kOffPart + (LN ? 2 * 2 * BM * 8 : 0);  // float2 [2 acc][128 rows]
+  static constexpr int kOffPart = kOffBeta + (LN ? BN * 4 : 0);  // float2 [2 acc][EW / 4 groups][128 rows]
+  static constexpr int kOffRecv = kOffPart + (LN ? 2 * (EW / 4) * BM * 8 : 0);  // float2 [2 acc][128 rows]
   static constexpr int kOffBar = kOffRecv + (LN ? 2 * BM * 8 : 0);
-  // full[STAGES], empty[STAGES], tmem_full[2], tmem_empty[2], res[kEpiWarps][kBufs], xch[2], tmem ptr
-  static constexpr int kNumBars = 2 * STAGES + 4 + kEpiWarps * kBufs + 2;
+  // full[STAGES], empty[STAGES], tmem_full[2], tmem_empty[2], res[EW][kBufs], xch[2], tmem ptr
+  static constexpr int kNumBars = 2 * STAGES + 4 + EW * kBufs + 2;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes;
   static constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -110,7 +116,7 @@ __device__ __forceinline__ float apply_act(float x, int act) {
 // the two BN-column halves of the same 256 rows (N = 2 BN), so every row of the output lives in one
 // cluster and its LayerNorm statistics are combined across the pairs (section "LN epilogue" below).
 template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN, bool LNREG, int ACT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                         const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_r,
                         const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
@@ -119,7 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         int32_t late_wait) {
   // staging buffers per epilogue warp: the residual is TMA-prefetched into one per chunk (RESIDUAL,
   // staged LN), or the row segment lives in registers (LNREG) / there is no residual: one reused buffer
-  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : (LNREG ? 0 : 1)>;
+  constexpr int EW = epi_warps<LN, LNREG>();
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? BN * 4 / EW / BK : (LNREG ? 0 : 1), EW>;
   static_assert(!LN || (CL == 4 && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs with a residual");
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -129,8 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint64_t* res_bar = tmem_empty + 2;  // [kEpiWarps][kBufs]
-  uint64_t* xch_bar = res_bar + kEpiWarps * S::kBufs;  // [2 acc] partner's row partials landed (LN)
+  uint64_t* res_bar = tmem_empty + 2;  // [EW][kBufs]
+  uint64_t* xch_bar = res_bar + EW * S::kBufs;  // [2 acc] partner's row partials landed (LN)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(xch_bar + 2);
   if (threadIdx.x == 0) GTRACE(0);
 
@@ -159,14 +166,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_b);
     tma_prefetch_desc(&tm_c);
     if (RESIDUAL) tma_prefetch_desc(&tm_r);
-    for (int i = 0; i < kEpiWarps * S::kBufs; ++i) mbar_init(&res_bar[i], 1);
+    for (int i = 0; i < EW * S::kBufs; ++i) mbar_init(&res_bar[i], 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);   // (leader) one expect_tx arrive; both CTAs' bytes complete it
       mbar_init(&empty[s], 1);  // one (multicast) MMA commit
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], kEpiWarps * (PAIR ? 2 : 1));  // (leader) the epilogue warps of both CTAs
+      mbar_init(&tmem_empty[a], EW * (PAIR ? 2 : 1));  // (leader) the epilogue warps of both CTAs
       mbar_init(&xch_bar[a], 1);                               // LN: local arm + the partner's st.async bytes
     }
     fence_barrier_init();
@@ -289,12 +296,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t xch_remote0 = mapa_shared(&xch_bar[0], partner);
     const int n_half0 = half * BN;
     // this CTA's column half of bias / gamma / beta, once
-    for (int c = static_cast<int>(threadIdx.x) - 64; c < BN; c += 32 * kEpiWarps) {
+    for (int c = static_cast<int>(threadIdx.x) - 64; c < BN; c += 32 * EW) {
       sbias[c] = bias != nullptr ? bias[n_half0 + c] : __float2bfloat16_rn(0.f);
       sgamma[c] = ln_gamma[n_half0 + c];
       sbeta[c] = ln_beta[n_half0 + c];
     }
-    named_bar_sync(1, 32 * kEpiWarps);
+    named_bar_sync(1, 32 * EW);
     const float inv_n = 1.0f / static_cast<float>(N);
     constexpr int kSeg = S::kWarpCols;  // 128 columns per thread
     const bool v8_ok = ((reinterpret_cast<uintptr_t>(res_ptr) | reinterpret_cast<uintptr_t>(out_ptr)) & 31u) == 0;
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float2* pa = part + acc * 2 * BM;
       pa[hf * BM + row] = make_float2(s1, s2);
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(13);
-      named_bar_sync(1, 32 * kEpiWarps);  // both column quarters of every row are in `part`
+      named_bar_sync(1, 32 * EW);  // both column quarters of every row are in `part`
       const float2 p0 = pa[row], p1 = pa[BM + row];
       const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial
       if (hf == 0)
@@ -446,12 +453,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t xch_remote0 = mapa_shared(&xch_bar[0], partner);
     const int n_half0 = half * BN;
     // this CTA's column half of bias / gamma / beta, once
-    for (int c = static_cast<int>(threadIdx.x) - 64; c < BN; c += 32 * kEpiWarps) {
+    for (int c = static_cast<int>(threadIdx.x) - 64; c < BN; c += 32 * EW) {
       sbias[c] = bias != nullptr ? bias[n_half0 + c] : __float2bfloat16_rn(0.f);
       sgamma[c] = ln_gamma[n_half0 + c];
       sbeta[c] = ln_beta[n_half0 + c];
     }
-    named_bar_sync(1, 32 * kEpiWarps);
+    named_bar_sync(1, 32 * EW);
     const float inv_n = 1.0f / static_cast<float>(N);
     int acc = 0;
     uint32_t acc_phase = 0, res_phase = 0;
@@ -470,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tmem_full[acc], acc_phase);
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
+      if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 4) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
@@ -506,11 +514,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_shared_v4(sbase + sw128_offset(lane, ch), o[0], o[1], o[2], o[3]);
         }
       }
-      float2* pa = part + acc * 2 * BM;
+      float2* pa = part + acc * (EW / 4) * BM;
       pa[hf * BM + row] = make_float2(s1, s2);
-      named_bar_sync(1, 32 * kEpiWarps);  // both column quarters of every row are in `part`
-      const float2 p0 = pa[row], p1 = pa[BM + row];
-      const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial
+      named_bar_sync(1, 32 * EW);  // every column group of every row is in `part`
+      float c1 = 0.f, c2 = 0.f;    // this CTA's 256-column partial
+#pragma unroll
+      for (int g = 0; g < EW / 4; ++g) {
+        const float2 pg = pa[g * BM + row];
+        c1 += pg.x;
+        c2 += pg.y;
+      }
       if (hf == 0)
         st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
       mbar_wait(&xch_bar[acc], acc_phase);
@@ -676,7 +689,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false, bool LNREG = false, int ACT = CORA_ACT_NONE>
 cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
-  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? 2 : (LNREG ? 0 : 1)>;
+  constexpr int EW = epi_warps<LN, LNREG>();
+  constexpr int kThreads = 64 + 32 * EW;
+  using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? BN * 4 / EW / BK : (LNREG ? 0 : 1), EW>;
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_2d_bf16(&ta, g.a, g.k, g.m, static_cast<uint64_t>(g.k) * 2, BK, BM, true) ||
       !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, CL > 1 ? BN / 2 : BN, true) ||
