@@ -14,7 +14,9 @@ import torch
 import synth
 import paper_2110_10221_b200 as P
 
-for lengths, d, H, dff in ((list(synth.C1_LENGTHS), 16, 2, 32), ([3, 130, 1, 64, 0, 7], 512, 8, 2048)):
+# the third batch (T ~ 12k) gives the fused GEMM + LN kernels several 256-row units per cluster
+for lengths, d, H, dff in ((list(synth.C1_LENGTHS), 16, 2, 32), ([3, 130, 1, 64, 0, 7], 512, 8, 2048),
+                           (list(synth.uniform_lengths(40, 100, 512, seed=5)), 512, 8, 2048)):
     T = int(np.sum(lengths))
     w = synth.encoder_weights(d, H, dff)
     params = P.EncoderParams.from_host(w)
