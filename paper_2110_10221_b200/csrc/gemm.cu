@@ -241,6 +241,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
           if (u == unit0 && kb == 0) GTRACE(3);
           if (u == unit0 && kb == k_blocks / 2) GTRACE(4);
           if (u == unit0 && kb == k_blocks - 1) GTRACE(5);
+#if defined(CORA_GEMM_TRACE) && CORA_GEMM_TRACE == 2
+          if (u == unit0 + unit_step && kb == 0) GTRACE(13);
+          if (u == unit0 + unit_step && kb == k_blocks - 1) GTRACE(14);
+#endif
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + S::kOffA + stage * S::kABytes);
           const uint32_t b_addr = smem_u32(smem + S::kOffB + stage * S::kBBytes);
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
         for (int e = 0; e < kSeg / 2; ++e) x |= vv[e];
         x = __reduce_or_sync(0xffffffffu, x);
         if (lane == 0) {
-          g_gemm_trace[blockIdx.x * 16 + 10] = x;
+          if (GTRACE_ON) g_gemm_trace[blockIdx.x * 16 + 10] = x;
           GTRACE(11);
         }
       }
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
         tmem_ld_wait();
 #ifdef CORA_GEMM_TRACE
         if (u == unit0 && ew == 0 && lane == 0) {  // the TMEM data has arrived
-          g_gemm_trace[blockIdx.x * 16 + 13 + c] = r[0] ^ r[63];
+          if (GTRACE_ON) g_gemm_trace[blockIdx.x * 16 + 13 + c] = r[0] ^ r[63];
           GTRACE(c == 0 ? 15 : 12);
         }
 #endif
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       }
       mbar_wait(&tmem_full[acc], acc_phase);
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
-      if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 4) GTRACE(10 + (u - unit0) / unit_step);
+      if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 2) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll 1

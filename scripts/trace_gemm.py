@@ -45,7 +45,7 @@ t0 = a[:, 0].min()
 rel = lambda k: (a[:, k] - t0) / 1000.0
 print(f"N={n} rank={rank} T={T}: {len(ctas)} CTAs traced; times in us from the first CTA entry")
 names = ["entry", "setup", "pdl_wait", "kb0", "kbK/2", "kblast", "acc", "xch", "stored", "exit_bar", "-", "res_in", "ldtm1", "pass1", "arrived", "ldtm0"]
-if os.environ.get("TRACE_UNITS"): names[11:15] = ["acc_u1", "acc_u2", "acc_u3", "acc_u4"]
+if os.environ.get("TRACE_UNITS"): names[11:15] = ["acc_u1", "acc_u2", "u1_kb0", "u1_kblast"]
 for k, nm in enumerate(names):
     v = rel(k)
     v = v[a[:, k] > 0]
