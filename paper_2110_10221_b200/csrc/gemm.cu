@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
           if (u == unit0 && kb == 0) GTRACE(3);
           if (u == unit0 && kb == k_blocks / 2) GTRACE(4);
           if (u == unit0 && kb == k_blocks - 1) GTRACE(5);
-#if defined(CORA_GEMM_TRACE) && CORA_GEMM_TRACE == 2
+#if defined(CORA_GEMM_TRACE)
           if (u == unit0 + unit_step && kb == 0) GTRACE(13);
           if (u == unit0 + unit_step && kb == k_blocks - 1) GTRACE(14);
 #endif
@@ -339,18 +339,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&xch_bar[acc], BM * 8);  // the partner's 128 row partials
       mbar_wait(&tmem_full[acc], acc_phase);
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
-#ifdef CORA_GEMM_TRACE
-      if (LNREG && u == unit0 && ew == 0) {  // the residual segments of every lane have arrived
-        uint32_t x = 0;
-#pragma unroll
-        for (int e = 0; e < kSeg / 2; ++e) x |= vv[e];
-        x = __reduce_or_sync(0xffffffffu, x);
-        if (lane == 0) {
-          if (GTRACE_ON) g_gemm_trace[blockIdx.x * 16 + 10] = x;
-          GTRACE(11);
-        }
-      }
-#endif
+      if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 2) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
       float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -360,17 +349,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
         CORA_TMEM_LD_32X32B_X32(taddr, r);
         CORA_TMEM_LD_32X32B_X32(taddr + 32, (r + 32));
         tmem_ld_wait();
-#ifdef CORA_GEMM_TRACE
-        if (u == unit0 && ew == 0 && lane == 0) {  // the TMEM data has arrived
-          if (GTRACE_ON) g_gemm_trace[blockIdx.x * 16 + 13 + c] = r[0] ^ r[63];
-          GTRACE(c == 0 ? 15 : 12);
-        }
-#endif
         if (c == kSeg / BK - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tmem_empty_lead0 + acc * 8);
-          if (u == unit0 && ew == 0 && lane == 0) GTRACE(14);
         }
         const uint32_t* bw = reinterpret_cast<const uint32_t*>(sbias + hf * kSeg + c * BK);
 #pragma unroll
@@ -388,7 +370,6 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       }
       float2* pa = part + acc * 2 * BM;
       pa[hf * BM + row] = make_float2(s1, s2);
-      if (u == unit0 && ew == 0 && lane == 0) GTRACE(13);
       named_bar_sync(1, 32 * EW);  // both column quarters of every row are in `part`
       const float2 p0 = pa[row], p1 = pa[BM + row];
       const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial

@@ -2,7 +2,8 @@
     CORA_LIB_PATH=variants/trace.so python scripts/trace_gemm.py [N] [rank]
 Stamps (globaltimer, ns, per CTA): 0 entry, 1 setup done, 2 after griddepcontrol.wait, 3/4/5 MMA issuer
 saw k-block 0 / K/2 / last of its first unit, 6 epilogue got the accumulator, 7 LN statistics exchanged,
-8 first unit stored, 9 before the exit cluster barrier, 10 after it, 11 residual segment arrived, 13 pass 1 done, 14 after the epilogue warps' barrier.
+8 first unit stored, 9 before the exit cluster barrier, 10 after it; 11 / 12 the accumulator of the
+second / third unit ready (LN kernels), 13 / 14 the MMA issuer saw k-block 0 / last of its second unit.
 """
 import ctypes
 import os
@@ -44,8 +45,8 @@ a = a[ctas]
 t0 = a[:, 0].min()
 rel = lambda k: (a[:, k] - t0) / 1000.0
 print(f"N={n} rank={rank} T={T}: {len(ctas)} CTAs traced; times in us from the first CTA entry")
-names = ["entry", "setup", "pdl_wait", "kb0", "kbK/2", "kblast", "acc", "xch", "stored", "exit_bar", "-", "res_in", "ldtm1", "pass1", "arrived", "ldtm0"]
-if os.environ.get("TRACE_UNITS"): names[11:15] = ["acc_u1", "acc_u2", "u1_kb0", "u1_kblast"]
+names = ["entry", "setup", "pdl_wait", "kb0", "kbK/2", "kblast", "acc", "xch", "stored", "exit_bar", "exit",
+         "acc_u1", "acc_u2", "u1_kb0", "u1_kblast", "-"]
 for k, nm in enumerate(names):
     v = rel(k)
     v = v[a[:, k] > 0]
