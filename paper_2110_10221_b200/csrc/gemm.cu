@@ -194,6 +194,24 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
   // late_wait: the operands were complete before the previous kernel (the prelude) started, so wait for
   // that kernel only at the end -- this grid then still completes after it (its dependents see both)
   if (threadIdx.x == 0) GTRACE(1);
+  // The weights (B) are never written by another kernel of the layer: the producer issues the B tiles of
+  // its first stages before griddepcontrol.wait, so they are in flight while the previous kernel drains
+  int pre_b = 0;
+  if (warp == 0 && lane == 0 && unit0 < num_units) {
+    pre_b = STAGES < k_blocks ? STAGES : k_blocks;
+    const int n0 = unit_n0(unit0);
+    for (int kb = 0; kb < pre_b; ++kb) {
+      uint8_t* sb = smem + S::kOffB + kb * S::kBBytes;
+      if (PAIR) {
+        const uint32_t bar = mapa_shared(&full[kb], lead_rank);
+        if (leader) mbar_arrive_expect_tx(&full[kb], 2 * S::kStageBytes);
+        tma_load_2d_cg2(sb, &tm_b, bar, kb * BK, n0 + static_cast<int>(prank) * (BN / 2));
+      } else {
+        mbar_arrive_expect_tx(&full[kb], S::kStageBytes);
+        tma_load_2d(sb, &tm_b, &full[kb], kb * BK, n0);
+      }
+    }
+  }
   if (!late_wait) pdl_wait();  // the previous kernel's outputs (our A / residual) are complete and visible
   if (threadIdx.x == 0) GTRACE(2);
   pdl_trigger();
@@ -206,19 +224,20 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       for (int u = unit0; u < num_units; u += unit_step) {
         const int m0 = unit_m0(u), n0 = unit_n0(u);
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          const bool b_issued = u == unit0 && kb < pre_b;  // fresh stage, B already in flight
+          if (!b_issued) mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + S::kOffA + stage * S::kABytes;
           uint8_t* sb = smem + S::kOffB + stage * S::kBBytes;
           if (PAIR) {
             // both CTAs' A rows and B halves complete the pair leader's full barrier
             const uint32_t bar = mapa_shared(&full[stage], lead_rank);
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::kStageBytes);
+            if (leader && !b_issued) mbar_arrive_expect_tx(&full[stage], 2 * S::kStageBytes);
             tma_load_2d_cg2(sa, &tm_a, bar, kb * BK, m0);
-            tma_load_2d_cg2(sb, &tm_b, bar, kb * BK, n0 + static_cast<int>(prank) * (BN / 2));
+            if (!b_issued) tma_load_2d_cg2(sb, &tm_b, bar, kb * BK, n0 + static_cast<int>(prank) * (BN / 2));
           } else {
-            mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+            if (!b_issued) mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
             tma_load_2d(sa, &tm_a, &full[stage], kb * BK, m0);
-            tma_load_2d(sb, &tm_b, &full[stage], kb * BK, n0);
+            if (!b_issued) tma_load_2d(sb, &tm_b, &full[stage], kb * BK, n0);
           }
           if (++stage == STAGES) stage = 0, phase ^= 1;
         }
