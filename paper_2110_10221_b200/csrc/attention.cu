@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else {
     // ------------------------------------------------------------ softmax / correction / epilogue
     const uint32_t qd = warp & 3;  // TMEM lane quadrant
+    const bool out_v8 = (reinterpret_cast<uintptr_t>(out) & 31u) == 0 && (d_model % 16) == 0 && (HD % 16) == 0;
     const int i = qd * 32 + lane;  // query row within the tile
     const uint32_t t_lane = (qd * 32) << 16;
     uint32_t s_ph = 0, pv_ph = 0;
@@ -458,12 +459,24 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int qrow = cur.qt * TQ + i;
         if (qrow < L) {
           const float inv = 1.f / l;
-          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD);
+          __nv_bfloat16* orow = out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD;
+          if (out_v8) {  // 32-B stores: one full sector per lane
   #pragma unroll
-          for (int g = 0; g < HD / 8; ++g) {
-            const float* o = reinterpret_cast<const float*>(orr) + g * 8;
-            dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
-                                pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+            for (int g = 0; g < HD / 16; ++g) {
+              const float* o = reinterpret_cast<const float*>(orr) + g * 16;
+              uint32_t w[8];
+  #pragma unroll
+              for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(o[2 * e] * inv, o[2 * e + 1] * inv);
+              st_global_v8(orow + g * 16, w);
+            }
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow);
+  #pragma unroll
+            for (int g = 0; g < HD / 8; ++g) {
+              const float* o = reinterpret_cast<const float*>(orr) + g * 8;
+              dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
+                                  pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+            }
           }
         }
       }
