@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kVThreads, 1)
   } else {
     // epilogue: quadrant q = warp % 4 -> accumulator rows [32 q, 32 q + 32)
     const uint32_t q = warp & 3;
+    const bool c_v8 = (reinterpret_cast<uintptr_t>(c) & 31u) == 0 && (ldc % 16) == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -208,7 +209,17 @@ __global__ void __launch_bounds__(kVThreads, 1)
         CORA_TMEM_LD_32X32B_X32(tmem_base + ((q * 32) << 16) + acc * VN + cb * 32, r);
         tmem_ld_wait();
         const int col0 = w.n0 + cb * 32;
-        if (row < pm && col0 < pn) {
+        if (row < pm && col0 < pn && c_v8 && col0 + 32 <= pn) {
+          // 32-B stores: one full sector per lane
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const float* v = reinterpret_cast<const float*>(r) + g * 16;
+            uint32_t wv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) wv[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+            st_global_v8(crow + col0 + g * 16, wv);
+          }
+        } else if (row < pm && col0 < pn) {
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const int col = col0 + g * 8;
