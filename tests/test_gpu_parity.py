@@ -215,6 +215,41 @@ def test_linear_residual_layernorm_with_activation(act):
     assert rel_err(to_np(c), ref) <= TOL_BF16
 
 
+def _misaligned_bf16(shape, values=None):
+    # a view whose base is 16-B but not 32-B aligned: the kernels' 32-B (v8) accesses must fall back
+    n = int(np.prod(shape))
+    buf = torch.empty(n + 16, dtype=torch.bfloat16, device="cuda")
+    base = (-(buf.data_ptr() // 2)) % 16  # elements to the next 32-B boundary
+    v = buf[base + 8: base + 8 + n].view(*shape)
+    assert v.data_ptr() % 32 == 16
+    if values is not None:
+        v.copy_(torch.as_tensor(values, dtype=torch.float32).to(torch.bfloat16))
+    return v
+
+
+def test_linear_residual_layernorm_16b_aligned_pointers():
+    m, k, n = 1000, 2048, 512  # the register-LN kernel (K >= 1024): 32-B residual loads / output stores
+    a = synth.round_bf16(synth.normal((m, k), 53))
+    w = synth.round_bf16(synth.normal((n, k), 54) / math.sqrt(k))
+    r = synth.round_bf16(synth.normal((m, n), 55))
+    g = synth.round_f32(1 + 0.1 * synth.normal((n,), 56))
+    be = synth.round_f32(0.1 * synth.normal((n,), 57))
+    out = _misaligned_bf16((m, n))
+    c = P().linear_residual_layernorm(bf16_cuda(a), bf16_cuda(w), _misaligned_bf16((m, n), r), f32_cuda(g),
+                                      f32_cuda(be), out=out)
+    ref = oracle.layernorm(oracle.linear(a, w, None, residual=r), g, be)
+    assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
+def test_attention_16b_aligned_output():
+    lengths = [130, 7, 64]
+    H, hd = 8, 64
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * H * hd), 58))
+    out = _misaligned_bf16((sum(lengths), H * hd))
+    o = P().ragged_attention(_layout(lengths, H), bf16_cuda(qkv), hd, out=out)
+    assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, H)) <= TOL_BF16
+
+
 def test_linear_residual_layernorm_unsupported_shape():
     a = bf16_cuda(synth.normal((300, 64), 1))
     w = bf16_cuda(synth.normal((256, 64), 2))
