@@ -155,6 +155,19 @@ def test_ragged_softmax_bf16_vector_path(lengths, H):
     assert rel_err(to_np(y), oracle.ragged_softmax(x, lengths, H)) <= TOL_BF16
 
 
+@pytest.mark.parametrize("H", [1, 3, 8])
+def test_ragged_softmax_bf16_token_path(H):
+    # T >= 4096: a warp per token, its H rows pipelined (rows at arbitrary offsets, empty sequences)
+    lengths = [int(v) for v in synth.uniform_lengths(40, 0, 260, seed=21)] + [512, 1, 0, 7]
+    assert sum(lengths) >= 4096
+    d = 8 * H
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 14))
+    x = synth.round_bf16(oracle.attention_scores_ragged(qkv, lengths, H))
+    lay = _layout(lengths, H)
+    y = P().ragged_softmax(lay, bf16_cuda(x))
+    assert rel_err(to_np(y), oracle.ragged_softmax(x, lengths, H)) <= TOL_BF16
+
+
 # ---------------------------------------------------------------- a2/a4/a6/a7: tcgen05 GEMM
 GEMM_SHAPES = [
     (128, 256, 64), (300, 1536, 512), (1000, 512, 2048), (257, 2048, 512), (16, 48, 16), (16, 16, 32),
