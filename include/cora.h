@@ -208,10 +208,12 @@ size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t
  * host->device, builds the layout (step a1), runs the layer (a2..a8) and copies y_host[T, d] back,
  * all ordered after prior work on `stream` and before later work on it (asynchronous when the host
  * buffers are pinned; the caller synchronises the stream before reading y_host).  For T >= 8192 the
- * batch is cut (on the host, from lengths_host) into 4 (T >= 16384: 8) contiguous sequence ranges that
+ * batch is cut (on the host, from lengths_host) into 4 (T >= 16384: 8; T >= 32768: 16) contiguous
+ * sequence ranges that
  * are copied in, computed and copied out as a pipeline over the caller's stream and two library-owned
  * side streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the layer on chunk c); each chunk is a
- * ragged batch of its own, so every row is computed exactly as in the one-shot path.  The side streams
+ * ragged batch of its own, so every row is computed as in the one-shot path (bitwise, except that
+ * sequences of < 128 tokens may be packed into different attention windows).  The side streams
  * and events are created once per device; concurrent calls from several host threads on one device are
  * not supported.  The device status word is not read (no hidden sync): call cora_layout_status on
  * *layout_out (the whole batch's layout, built on `stream`) after synchronising to detect data errors

@@ -506,7 +506,7 @@ size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t
 namespace {
 // Side streams and events of the pipelined host forward, created once per device (never on the hot path
 // after the first call).
-constexpr int kMaxChunks = 8;
+constexpr int kMaxChunks = 16;
 struct HostPipe {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t start = nullptr, done = nullptr, h2d_ev[kMaxChunks] = {}, comp_ev[kMaxChunks] = {};
@@ -572,8 +572,12 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
     sum += lengths_host[b];
     bad |= lengths_host[b] < 0 || lengths_host[b] > max_len;
   }
-  int K = (bad || sum != total_tokens) ? 1 : total_tokens >= 16384 ? 8 : total_tokens >= 8192 ? 4 : 1;
-  if (const char* e = getenv("CORA_HOST_CHUNKS")) {  // experiments: force the chunk count (1..8)
+  int K = (bad || sum != total_tokens) ? 1
+          : total_tokens >= 32768 ? 16
+          : total_tokens >= 16384 ? 8
+          : total_tokens >= 8192  ? 4
+                                  : 1;
+  if (const char* e = getenv("CORA_HOST_CHUNKS")) {  // experiments: force the chunk count (1..16)
     const int k = atoi(e);
     if (k >= 1 && k <= kMaxChunks && !bad && sum == total_tokens) K = k;
   }
