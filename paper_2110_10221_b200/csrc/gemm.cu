@@ -14,7 +14,7 @@
 // flight (smem stages) cover the ~2 us TMA latency with half the bytes.
 //   warp 0      : TMA producer (both CTAs; the leader's `full` barrier collects both CTAs' bytes)
 //   warp 1      : TMEM allocator (both CTAs) + single-thread tcgen05.mma issuer (leader only)
-//   warps 2..9  : epilogue, two warps per TMEM lane quadrant (column halves): tcgen05.ld -> +bias
+//   warps 2..9  : epilogue (2..17 for the staged LN), two (four) warps per TMEM lane quadrant: tcgen05.ld -> +bias
 //                 (smem) -> act -> +residual (TMA-loaded into the swizzled staging buffer) -> bf16 in
 //                 place -> TMA store (32 rows x 64 cols per chunk)
 //   TMEM holds two BN-column fp32 accumulators so the epilogue of tile i overlaps the main loop of
@@ -22,9 +22,13 @@
 // The mainloop is bound by the bytes in flight (stages x stage bytes / TMA latency): non-residual GEMMs
 // keep one reused staging buffer per epilogue warp and 6 stages.
 // LN (N = 512, steps a4+a5 / a7+a8): two CTA pairs of one 4-CTA cluster hold the two 256-column halves
-// of the same 256 rows and combine LayerNorm row statistics over DSMEM.  Short K (out-proj, epilogue-
-// bound): residual TMA-staged, 4 stages.  Long K (FF2, mainloop-bound): LNREG -- row segments in
-// registers, rows stored straight to global memory, 6 stages.
+// of the same 256 rows and combine LayerNorm row statistics over DSMEM.  Short K (out-proj, bound by
+// shared-memory bandwidth): residual TMA-staged, 4 stages, 16 epilogue warps (64 columns each).  Long K
+// (FF2, mainloop-bound): LNREG -- row segments in registers, 32-B residual loads and output stores,
+// 6 stages.  The LN kernels have no activation variants (one epilogue body),
+// the plain GEMM takes the activation as a template parameter.
+// PDL: the producer issues the weight (B) tiles of its first stages before griddepcontrol.wait -- no
+// kernel of the layer writes the weights -- and A / residual only after it.
 #include <cuda_bf16.h>
 
 #include <cstdint>
