@@ -476,6 +476,7 @@ def test_encoder_stack(n_layers, lengths, d, H, dff):
     [3, 130, 1, 64],                                        # one chunk
     list(synth.uniform_lengths(40, 129, 512, seed=11)),     # T >= 8192: 4 chunks over 3 streams
     list(synth.dataset_lengths("wiki512", 64)),             # chunks + short-sequence windows
+    list(synth.uniform_lengths(120, 260, 512, seed=12)),    # T >= 32768: 16 chunks
 ], ids=lambda l: f"B{len(l)}-T{sum(l)}")
 def test_forward_host_matches_device_path(lengths):
     d, H, dff = 512, 8, 2048
