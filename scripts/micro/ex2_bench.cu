@@ -1,0 +1,93 @@
+// Microbenchmark: MUFU.EX2 throughput on this B200 (the roofline denominator of the attention kernel,
+// reported as "bound": "alu"), and the attention softmax inner-loop mix (FFMA2 + 2 MUFU.EX2 + FADD2 +
+// F2FP per key pair) at 1..8 warps per SM sub-partition.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ex2_bench ex2_bench.cu && ./ex2_bench
+#include <cuda_bf16.h>
+#include <cstdio>
+#include <cstdint>
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// pure EX2: 16 independent chains per thread
+__global__ void k_ex2(float* out, int iters, float seed) {
+  float v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = seed * (threadIdx.x + k) * 1e-6f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = ex2(v[k]) * -0.5f;  // FMUL keeps values bounded (one FMA-pipe op per EX2)
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += v[k];
+  if (s == 1234.5f) out[threadIdx.x] = s;
+}
+
+// softmax mix: for 64 key pairs: x = fma2(s, scale, -m); p = ex2 x 2; r += p (FADD2); pack bf16x2
+__global__ void k_mix(float* out, int iters, float seed) {
+  float s[128];
+#pragma unroll
+  for (int k = 0; k < 128; ++k) s[k] = seed * (threadIdx.x ^ k) * 1e-3f;
+  float2 r2[4] = {};
+  uint32_t acc = 0;
+  const float2 sc = make_float2(0.18f, 0.18f);
+  float m = 0.25f;
+  for (int it = 0; it < iters; ++it) {
+    const float2 nm = make_float2(-m, -m);
+#pragma unroll
+    for (int c = 0; c < 128; c += 2) {
+      const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc, nm);
+      const float p0 = ex2(x.x), p1 = ex2(x.y);
+      r2[(c >> 1) & 3] = __fadd2_rn(r2[(c >> 1) & 3], make_float2(p0, p1));
+      uint32_t pk;
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(p1), "f"(p0));
+      acc ^= pk;
+    }
+    m += 1e-7f * r2[0].x;
+  }
+  if (acc == 0x12345u) out[threadIdx.x] = r2[0].x + r2[1].y + r2[2].x + r2[3].y;
+}
+
+int main() {
+  int dev = 0, sms = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  float* out;
+  cudaMalloc(&out, 4096 * sizeof(float));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int wps : {4, 8, 16, 32}) {  // warps per SM (1 CTA of wps warps per SM)
+    const int iters = 4096;
+    k_ex2<<<sms, 32 * wps>>>(out, 16, 1.f);
+    cudaEventRecord(a);
+    k_ex2<<<sms, 32 * wps>>>(out, iters, 1.f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double n = double(sms) * 32 * wps * iters * 16;
+    printf("{\"bench\": \"ex2\", \"warps_per_sm\": %d, \"gex2_per_s\": %.1f, \"ex2_per_clk_per_sm_at_max_clock\": %.2f}\n",
+           wps, n / ms / 1e6, n / (ms * 1e-3) / sms / (clk * 1e3));
+  }
+  for (int wps : {4, 8, 12, 16}) {
+    const int iters = 512;
+    k_mix<<<sms, 32 * wps>>>(out, 8, 1.f);
+    cudaEventRecord(a);
+    k_mix<<<sms, 32 * wps>>>(out, iters, 1.f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double n = double(sms) * 32 * wps * iters * 128;
+    printf("{\"bench\": \"softmax_mix\", \"warps_per_sm\": %d, \"gex2_per_s\": %.1f, \"ex2_per_clk_per_sm_at_max_clock\": %.2f}\n",
+           wps, n / ms / 1e6, n / (ms * 1e-3) / sms / (clk * 1e3));
+  }
+  printf("{\"sms\": %d, \"max_clock_mhz\": %.0f}\n", sms, clk / 1e3);
+  return 0;
+}

@@ -309,6 +309,39 @@ def test_ragged_masked_attention(lengths, head_dim, heads):
     assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, heads, causal=True)) <= TOL_BF16
 
 
+def _rescale_qkv(lengths, H, hd, seed):
+    """QKV whose row maxima move by far more than the kernel's lazy-rescale threshold (2^8, reading a3-r1)
+    in KV tiles j >= 1: Q scaled by 4, and the keys of KV tile j of every sequence by 1 + 1.5 j, so the
+    logit spread grows tile by tile (tile 0: ~14 log2 units, tile 1: ~36, tile 3: ~79)."""
+    d = H * hd
+    qkv = synth.normal((sum(lengths), 3 * d), seed)
+    qkv[:, :d] *= 4.0
+    r0 = 0
+    for L in lengths:
+        pos = np.arange(L)
+        qkv[r0:r0 + L, d:2 * d] *= (1.0 + 1.5 * (pos // 128))[:, None]
+        r0 += L
+    return synth.round_bf16(qkv)
+
+
+@pytest.mark.parametrize("lengths", [[129], [300], [512], [129, 300, 512, 7, 450]], ids=lambda l: f"L{'-'.join(map(str, l))}")
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_forced_lazy_rescale(lengths, causal):
+    """The in-TMEM O rescale branch (a later KV tile exceeds the reference max by > 8 log2 units) against
+    the exact fp64 definition (exact on valid rows)."""
+    H, hd = 8, 64
+    qkv = _rescale_qkv(lengths, H, hd, 41)
+    # the construction really moves the max by > 8 log2 units after the first KV tile
+    d = H * hd
+    q, k = qkv[:lengths[0], :hd], qkv[:lengths[0], d:d + hd]
+    s = (q @ k.T) / 8.0 * 1.4426950408889634
+    if lengths[0] > 128:
+        assert (s[:, 128:].max(1) - s[:, :128].max(1)).max() > 8.0
+    lay = _layout(lengths, H)
+    o = P().ragged_attention(lay, bf16_cuda(qkv), hd, causal=causal)
+    assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, H, causal=causal)) <= TOL_BF16
+
+
 def test_attention_poisoned_output_untouched_rows_none():
     # every output row belongs to some sequence: all are written; NaN-poison must disappear
     lengths = [5, 0, 129, 64]
