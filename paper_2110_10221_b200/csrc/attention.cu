@@ -33,7 +33,6 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
-#include <type_traits>
 
 #include "cora_internal.h"
 #include "ptx.cuh"
@@ -47,13 +46,7 @@ constexpr int TK = 128;       // keys per KV tile
 constexpr int QSTAGES = 2;    // Q double buffer: the next tile's Q streams in under the current tile
 constexpr int KSTAGES = 3;    // K ring depth
 constexpr int VSTAGES = 2;    // V ring depth
-// warps 0-3: softmax (warp w reads TMEM lanes 32w..32w+31), warp 4: TMA producer, warp 5: TMEM allocator +
-// MMA issuer, warps 6-7: idle (they complete warpgroup 1, whose registers go to the softmax warpgroup)
-constexpr int kThreads = 256;
-constexpr uint32_t kProducerWarp = 4, kMmaWarp = 5;
-// 2 CTAs x 256 threads x 128 registers at launch; setmaxnreg moves them to 200 (softmax) / 56 (others):
-// 128 x 200 + 128 x 56 = 256 x 128
-constexpr uint32_t kRegsSoftmax = 200, kRegsOther = 56;
+constexpr int kThreads = 192;
 constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
 // Lazy rescaling (reading a3-r1): the running reference max m_ref of a row is only
 // moved when a new score exceeds it by more than kRescaleLog2 (in log2 units), so P <= 2^8 and the
@@ -79,26 +72,6 @@ __device__ __forceinline__ float exp2_poly(float x) {
   const float p = fmaf(fmaf(fmaf(0.053027520f, f, 0.24221394f), f, 0.69357257f), f, 0.99995904f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
-
-#ifdef CORA_ATTN_TRACE
-// Phase trace (profiling builds only): softmax warp 0 lane 0 and the MMA thread of the first kTraceCtas
-// CTAs record (clock64 << 8 | event) into a per-CTA, per-role ring of kTraceLen entries.
-constexpr int kTraceCtas = 296, kTraceLen = 2048;
-__device__ uint64_t g_attn_trace[kTraceCtas][2][kTraceLen];
-__device__ int g_attn_trace_n[kTraceCtas][2];
-#define ATR(role, ev)                                                                              \
-  do {                                                                                            \
-    if (blockIdx.x < kTraceCtas && atr_n < kTraceLen)                                             \
-      g_attn_trace[blockIdx.x][role][atr_n++] = (clock64() << 8) | (ev);                          \
-  } while (0)
-#define ATR_DONE(role) do { if (blockIdx.x < kTraceCtas) g_attn_trace_n[blockIdx.x][role] = atr_n; } while (0)
-#define ATR_SM(ev) do { if (qd == 0 && lane == 0) ATR(0, ev); } while (0)
-#define ATR_MMA(ev) ATR(1, ev)
-#else
-#define ATR_SM(ev) do {} while (0)
-#define ATR_MMA(ev) do {} while (0)
-#define ATR_DONE(role) do {} while (0)
-#endif
 
 struct AttnSmem {
   static constexpr int kOffQ = 0;
@@ -147,50 +120,9 @@ __device__ __forceinline__ WorkUnit load_work(const int32_t* list, const int2* l
   return WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2, t.packed};
 }
 
-// Deferred epilogue helpers (softmax warps): read the finished O accumulator of this warp's 32 rows out of
-// TMEM (its last PV has completed) and release the accumulator to the next tile's PV_0; normalise and store
-// a row.
-__device__ __forceinline__ void read_pending_o(uint32_t (&orr)[HD], uint64_t* o_empty, uint32_t taddr_o, uint32_t lane) {
-  CORA_TMEM_LD_32X32B_X32(taddr_o, orr);
-  CORA_TMEM_LD_32X32B_X32(taddr_o + 32, (orr + 32));
-  tmem_ld_wait();
-  tc_fence_before();
-  __syncwarp();
-  if (lane == 0) mbar_arrive(o_empty);
-}
-__device__ __forceinline__ void store_o(const uint32_t (&orr)[HD], __nv_bfloat16* out, int32_t d_model, bool out_v8,
-                                        int row, int col, float lsum) {
-  if (row < 0) return;
-  const float inv = 1.f / lsum;
-  __nv_bfloat16* orow = out + static_cast<size_t>(row) * d_model + col;
-  if (out_v8) {  // 32-B stores: one full sector per lane
-#pragma unroll
-    for (int g = 0; g < HD / 16; ++g) {
-      const float* o = reinterpret_cast<const float*>(orr) + g * 16;
-      uint32_t w[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(o[2 * e] * inv, o[2 * e + 1] * inv);
-      st_global_v8(orow + g * 16, w);
-    }
-  } else {
-    uint4* dst = reinterpret_cast<uint4*>(orow);
-#pragma unroll
-    for (int g = 0; g < HD / 8; ++g) {
-      const float* o = reinterpret_cast<const float*>(orr) + g * 8;
-      dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
-                          pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
-    }
-  }
-}
-
 // CAUSAL: masked MHA (App. D.3): query i attends to keys j <= i of its sequence, so
 // q-tile qt needs only KV tiles j <= qt (the "lower triangular" ragged loop -- tiles above the diagonal
 // are never loaded or computed) and the diagonal tile is masked per element.
-//
-// Per KV step the work is cut to the keys that exist: a step over `valid` < 128 keys (the tail tile of a
-// sequence, a packed window, the diagonal tile of a causal q-tile) computes S with N = 32 * ceil(valid/32)
-// columns, the softmax warps load / exponentiate only those 32-key chunks (and, on a causal diagonal,
-// only the chunks up to their own rows), and the PV MMA reduces over ceil(valid/16) 16-key steps.
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
@@ -218,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const uint32_t warp = warp_id(), lane = lane_id();
 
-  if (warp == kProducerWarp && lane == 0) {
+  if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     for (int s = 0; s < QSTAGES; ++s) {
       mbar_init(&q_full[s], 1);
@@ -239,162 +171,129 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(o_empty, 4);
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<kTmemCols>(tmem_ptr);
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_ptr);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr;
   pdl_wait();  // QKV (previous kernel) complete and visible
   pdl_trigger();
-  // tmem_base / n_tiles are read after the register reallocation of each role (values live across
-  // setmaxnreg are spilled by ptxas)
+  const int n_tiles = *n_tiles_ptr;
+  // every role walks the same tiles; the next tile's metadata load is issued one tile ahead
+  WorkUnit wu_next{};
+  if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
 
-  if (warp >= 4) {
-    // warpgroup 1 (producer, MMA issuer, two idle warps) hands its registers to the softmax warpgroup
-    setmaxnreg_dec<kRegsOther>();
-    const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
-    const int n_tiles = *n_tiles_ptr;
-    // every role walks the same tiles; the next tile's metadata load is issued one tile ahead
-    WorkUnit wu_next{};
-    if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
-    if (warp == kProducerWarp) {
-      // ------------------------------------------------------------ TMA producers
-      // lane 0 streams Q and K, lane 1 streams V: the two rings are refilled independently, so a V slot
-      // still held by a pending PV never delays the next K load (and vice versa)
-      if (lane == 0) {
-        uint32_t q_ph = 0, k_ph = 0;
-        int qs = 0, ks = 0;
-        for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-          const WorkUnit wu = wu_next;
-          if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
-          for (int sub = 0; sub < wu.count; ++sub) {
-            const WorkTile cur = wu.tile(sub);
-            const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
-            mbar_wait<false>(&q_empty[qs], q_ph ^ 1);
-            mbar_arrive_expect_tx(&q_full[qs], kTileBytes);
-            tma_load_2d(smem + AttnSmem::kOffQ + qs * kTileBytes, &tm_qkv, &q_full[qs], cur.h * HD, cur.r0 + cur.qt * TQ);
-            if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
-            for (int j = 0; j < nkv; ++j) {
-              mbar_wait<false>(&k_empty[ks], k_ph ^ 1);
-              mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
-              tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
-                          cur.r0 + j * TK);
-              if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-            }
-          }
-        }
-      } else if (lane == 1) {
-        uint32_t v_ph = 0;
-        int vs = 0;
-        for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-          const WorkUnit wu = wu_next;
-          if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
-          for (int sub = 0; sub < wu.count; ++sub) {
-            const WorkTile cur = wu.tile(sub);
-            const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
-            for (int j = 0; j < nkv; ++j) {
-              mbar_wait<false>(&v_empty[vs], v_ph ^ 1);
-              mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
-              tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
-                          cur.r0 + j * TK);
-              if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
-            }
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producers
+    // lane 0 streams Q and K, lane 1 streams V: the two rings are refilled independently, so a V slot
+    // still held by a pending PV never delays the next K load (and vice versa)
+    if (lane == 0) {
+      uint32_t q_ph = 0, k_ph = 0;
+      int qs = 0, ks = 0;
+      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+        const WorkUnit wu = wu_next;
+        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
+          mbar_wait<false>(&q_empty[qs], q_ph ^ 1);
+          mbar_arrive_expect_tx(&q_full[qs], kTileBytes);
+          tma_load_2d(smem + AttnSmem::kOffQ + qs * kTileBytes, &tm_qkv, &q_full[qs], cur.h * HD, cur.r0 + cur.qt * TQ);
+          if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
+          for (int j = 0; j < nkv; ++j) {
+            mbar_wait<false>(&k_empty[ks], k_ph ^ 1);
+            mbar_arrive_expect_tx(&k_full[ks], kTileBytes);
+            tma_load_2d(smem + AttnSmem::kOffK + ks * kTileBytes, &tm_qkv, &k_full[ks], d_model + cur.h * HD,
+                        cur.r0 + j * TK);
+            if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
           }
         }
       }
-    } else if (warp == kMmaWarp) {
-      // ------------------------------------------------------------ MMA issuer (one thread)
-      if (lane == 0) {
-        constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HD, /*b_mn_major=*/true);
-#ifdef CORA_ATTN_TRACE
-        int atr_n = 0;
-#endif
-        int qs = 0, ks = 0, vs = 0;
-        uint32_t q_ph = 0, k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
-        for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-          const WorkUnit wu = wu_next;
-          if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
-          for (int sub = 0; sub < wu.count; ++sub) {
-            const WorkTile cur = wu.tile(sub);
-            const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
-            mbar_wait<false>(&q_full[qs], q_ph);
-            const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
-            auto issue_s = [&](int j) {
-              // N = the 32-key chunks that hold keys of the sequence (the softmax warps read no others)
-              const int valid = min(cur.L - j * TK, TK);
-              const uint32_t idesc_s = make_idesc_bf16(TQ, static_cast<uint32_t>((valid + 31) & ~31));
-              ATR_MMA(20);
-              mbar_wait<false>(&k_full[ks], k_ph);
-              ATR_MMA(21);
-              mbar_wait<false>(s_empty, s_ph ^ 1);
-              ATR_MMA(22);
-              s_ph ^= 1;
-              tc_fence_after();
-              const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
-  #pragma unroll
-              for (int k = 0; k < HD / 16; ++k)
-                umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
-                             make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
-              umma_commit(&k_empty[ks]);
-              umma_commit(s_full);
-              if (j + 1 == nkv) umma_commit(&q_empty[qs]);  // Q slot free once the last S of the tile is done
-              if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-            };
-            issue_s(0);
-            for (int j = 0; j < nkv; ++j) {
-              if (j + 1 < nkv) issue_s(j + 1);  // S_{j+1} overlaps the softmax of S_j
-              mbar_wait<false>(p_full, p_ph);   // P_j in TMEM (and O rescaled if needed)
-              ATR_MMA(23);
-              p_ph ^= 1;
-              mbar_wait<false>(&v_full[vs], v_ph);
-              ATR_MMA(24);
-              if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
-                mbar_wait<false>(o_empty, o_ph ^ 1);
-                o_ph ^= 1;
-              }
-              ATR_MMA(25);
-              tc_fence_after();
-              const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV + vs * kTileBytes);
-              const int ksteps = (min(cur.L - j * TK, TK) + 15) >> 4;  // 16-key steps holding keys of the sequence
-              for (int k = 0; k < ksteps; ++k) {
-                // A = P from TMEM (16 keys = 8 packed columns per step), B = V (MN-major, 16 key rows per step)
-                const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
-                umma_bf16_ts(tmem_base + kTmemO, tmem_base + kTmemP + k * 8, vd, idesc_o, (j | k) != 0);
-              }
-              umma_commit(&v_empty[vs]);
-              umma_commit(pv_done);
-              if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
-            }
-            if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
+    } else if (lane == 1) {
+      uint32_t v_ph = 0;
+      int vs = 0;
+      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+        const WorkUnit wu = wu_next;
+        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
+          for (int j = 0; j < nkv; ++j) {
+            mbar_wait<false>(&v_empty[vs], v_ph ^ 1);
+            mbar_arrive_expect_tx(&v_full[vs], kTileBytes);
+            tma_load_2d(smem + AttnSmem::kOffV + vs * kTileBytes, &tm_qkv, &v_full[vs], 2 * d_model + cur.h * HD,
+                        cur.r0 + j * TK);
+            if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
           }
         }
-        ATR_DONE(1);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK);
+      constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HD, /*b_mn_major=*/true);
+      int qs = 0, ks = 0, vs = 0;
+      uint32_t q_ph = 0, k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
+      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
+        const WorkUnit wu = wu_next;
+        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
+          mbar_wait<false>(&q_full[qs], q_ph);
+          const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
+          auto issue_s = [&](bool last) {
+            mbar_wait<false>(&k_full[ks], k_ph);
+            mbar_wait<false>(s_empty, s_ph ^ 1);
+            s_ph ^= 1;
+            tc_fence_after();
+            const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
+  #pragma unroll
+            for (int k = 0; k < HD / 16; ++k)
+              umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
+                           make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
+            umma_commit(&k_empty[ks]);
+            umma_commit(s_full);
+            if (last) umma_commit(&q_empty[qs]);  // Q slot free once the last S of the tile is done
+            if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+          };
+          issue_s(nkv == 1);
+          for (int j = 0; j < nkv; ++j) {
+            if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
+            mbar_wait<false>(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
+            p_ph ^= 1;
+            mbar_wait<false>(&v_full[vs], v_ph);
+            if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
+              mbar_wait<false>(o_empty, o_ph ^ 1);
+              o_ph ^= 1;
+            }
+            tc_fence_after();
+            const uint32_t v_addr = smem_u32(smem + AttnSmem::kOffV + vs * kTileBytes);
+  #pragma unroll
+            for (int k = 0; k < TK / 16; ++k) {
+              // A = P from TMEM (16 keys = 8 packed columns per step), B = V (MN-major, 16 key rows per step)
+              const uint64_t vd = make_sdesc_sw128(v_addr + k * 16 * 128, kTileBytes, 1024);
+              umma_bf16_ts(tmem_base + kTmemO, tmem_base + kTmemP + k * 8, vd, idesc_o, (j | k) != 0);
+            }
+            umma_commit(&v_empty[vs]);
+            umma_commit(pv_done);
+            if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
+          }
+          if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
+        }
       }
     }
   } else {
     // ------------------------------------------------------------ softmax / correction / epilogue
-    setmaxnreg_inc<kRegsSoftmax>();
-    const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
-    const int n_tiles = *n_tiles_ptr;
-#ifdef CORA_ATTN_TRACE
-    int atr_n = 0;
-#endif
-    const uint32_t qd = warp;  // TMEM lane quadrant
+    const uint32_t qd = warp & 3;  // TMEM lane quadrant
     const bool out_v8 = (reinterpret_cast<uintptr_t>(out) & 31u) == 0 && (d_model % 16) == 0 && (HD % 16) == 0;
     const int i = qd * 32 + lane;  // query row within the tile
     const uint32_t t_lane = (qd * 32) << 16;
-    const float2 sc2 = make_float2(scale_log2, scale_log2);
     uint32_t s_ph = 0, pv_ph = 0;
-    // Deferred epilogue: the O of tile n is read out of TMEM only after the first exponentials of tile n+1
-    // (its last PV has completed by then) and stored after P_0 of tile n+1 is handed to the MMA warp, so
-    // neither the last-PV latency nor the global stores sit on the critical path.  pend_* describe the
-    // tile whose O is still in TMEM (pend_row < 0: nothing of it to store for this thread).
-    bool pend = false;
-    int pend_row = -1;  // packed output row of this thread's query in the pending tile, or -1
-    int pend_col = 0;   // first output column (head offset)
-    float pend_l = 1.f;
     // the next tile's metadata is prefetched one tile ahead into shared memory with cp.async (no
-    // registers held while in flight)
-    int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + qd * 2;  // [2 slots] per warp
+    // registers held while in flight; prefetching into registers spilled)
+    int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + (warp - 2) * 2;  // [2 slots] per warp
     auto prefetch_meta = [&](int idx, int slot) {
       if (lane == 0 && idx < n_tiles) {
         cp_async_4(&meta[slot].x, tiles + idx);
@@ -405,11 +304,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     int slot = 0;
     prefetch_meta(blockIdx.x, 0);
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x, slot ^= 1) {
-      ATR_SM(11);
       cp_async_wait_all();
       __syncwarp();
       const int4 mt = meta[slot];
-      ATR_SM(12);
       __syncwarp();
       prefetch_meta(idx + gridDim.x, slot ^ 1);
       WorkUnit wu;
@@ -425,9 +322,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int sub = 0; sub < wu.count; ++sub) {
         const WorkTile cur = wu.tile(sub);
         const int L = cur.L;
-        ATR_SM(9);
         const int nkv = CAUSAL ? min((L + TK - 1) / TK, cur.qt + 1) : (L + TK - 1) / TK;
-        const int qrow = cur.qt * TQ + i;
         if (cur.qt * TQ + static_cast<int>(qd) * 32 >= L) {
           // none of this warp's 32 query rows belongs to the sequence: keep the barrier protocol,
           // skip the math (its P rows are stale, its O rows are never stored)
@@ -438,183 +333,159 @@ __global__ void __launch_bounds__(kThreads, 2)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_empty);
-            if (j > 0 || pend) {  // PV_{j-1} (j == 0: the pending tile's last PV)
+            if (j > 0) {
               mbar_wait<false>(pv_done, pv_ph);
               pv_ph ^= 1;
-              tc_fence_after();
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
-            if (j == 0 && pend) {
-              uint32_t orr[HD];
-              read_pending_o(orr, o_empty, tmem_base + t_lane + kTmemO, lane);
-              store_o(orr, out, d_model, out_v8, pend_row, pend_col, pend_l);
-            }
           }
-          pend = true;
-          pend_row = -1;
+          mbar_wait<false>(pv_done, pv_ph);
+          pv_ph ^= 1;
+          tc_fence_after();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(o_empty);
           continue;
-        }
-        // keys [lo, hi) of a packed window belong to this row's sequence (f_fo / f_fi maps of the prelude)
-        int plo = 0, phi = 0;
-        if (cur.packed && i < L) {
-          const int t = cur.r0 + i;
-          plo = i - __ldg(pos_in_seq + t);
-          phi = plo + __ldg(lengths + __ldg(seq_of_tok + t));
         }
         float m_ref = -INFINITY, l = 0.f;
         for (int j = 0; j < nkv; ++j) {
-          const int valid = min(L - j * TK, TK);  // keys of this tile that belong to the sequence (>= 1)
-          const int ncm = (valid + 31) >> 5;      // 32-key chunks the S / PV MMAs cover
-          const bool diag = CAUSAL && j == cur.qt;
-          // chunks holding keys visible to this warp's rows (causal diagonal: keys <= row)
-          const int nc = diag ? min(ncm, static_cast<int>(qd) + 1) : ncm;
-          // visible keys of this row in the chunks computed: [lo, hi)
-          const int lo = cur.packed ? plo : 0;
-          int hi = cur.packed ? phi : valid;
-          if (CAUSAL && (diag || cur.packed)) hi = min(hi, i + 1);
-          ATR_SM(1);
+          const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
           mbar_wait<false>(s_full, s_ph);
-          ATR_SM(2);
           s_ph ^= 1;
           tc_fence_after();
-          bool bump = false;
-          float alpha = 1.f;
-          uint32_t pk[TK / 2];
-          auto softmax = [&](auto nc_tag) {
-            constexpr int NC = decltype(nc_tag)::value;
-            uint32_t sr[NC * 32];
-#pragma unroll
-            for (int cb = 0; cb < NC; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
-            tmem_ld_wait();
-            ATR_SM(3);
-            // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(s_empty);
-            float* sv = reinterpret_cast<float*>(sr);
-            // keys outside [lo, hi) get -inf before the row max (reading c18): a packed window masks every
-            // chunk, a tail / diagonal tile only its last computed chunk
-            if (cur.packed) {
-#pragma unroll
-              for (int c = 0; c < NC * 32; ++c)
-                if (c < lo || c >= hi) sv[c] = -INFINITY;
-            } else if (hi < NC * 32) {
-#pragma unroll
-              for (int c = (NC - 1) * 32; c < NC * 32; ++c)
-                if (c >= hi) sv[c] = -INFINITY;
+          uint32_t sr[TK];
+  #pragma unroll
+          for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
+          tmem_ld_wait();
+          // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty);
+          float* sv = reinterpret_cast<float*>(sr);
+          // row max over the valid keys (keys >= L_b masked to -inf in the tail tile; with CAUSAL also the
+          // keys after the query in the diagonal tile)
+          const bool masked = (CAUSAL && j == cur.qt) || valid < TK || cur.packed;
+          if (cur.packed) {  // block-diagonal (one KV tile: j == 0 == qt)
+            // keys [lo, hi) of the window belong to this row's sequence (f_fo / f_fi maps of the prelude)
+            int lo = 0, hi = 0;
+            if (i < L) {
+              const int t = cur.r0 + i;
+              lo = i - __ldg(pos_in_seq + t);
+              hi = lo + __ldg(lengths + __ldg(seq_of_tok + t));
             }
-            // row max: three-input max, four independent chains
-#ifdef CORA_ATTN_EXP_NOMAX
-            if (j == 0) {
-#endif
-            float m4[4] = {sv[0], sv[1], sv[2], sv[3]};
-#pragma unroll
-            for (int c = 4; c < NC * 32; c += 8) {
-              m4[0] = fmax3f(m4[0], sv[c], sv[c + 1]);
-              m4[1] = fmax3f(m4[1], sv[c + 2], sv[c + 3]);
-              if (c + 4 < NC * 32) {
-                m4[2] = fmax3f(m4[2], sv[c + 4], sv[c + 5]);
-                m4[3] = fmax3f(m4[3], sv[c + 6], sv[c + 7]);
-              }
-            }
-            const float mx = fmaxf(fmax3f(m4[0], m4[1], m4[2]), m4[3]) * scale_log2;
-            ATR_SM(4);
-            // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
-            bump = mx > m_ref + kRescaleLog2;
-            const float m_new = bump ? mx : m_ref;
-            alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
-            m_ref = m_new;
-#ifdef CORA_ATTN_EXP_NOMAX
-            }
-#endif
-            // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0); x for two keys per FFMA2, row
-            // sum for two keys per FADD2 (four chains), bf16 pairs packed right away (the A operand
-            // layout of the TS MMA: 2 keys per column)
-            const float2 nm2 = make_float2(-m_ref, -m_ref);
-            float2 r2[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) r2[k] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int c = 0; c < NC * 32; c += 2) {
-              const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sc2, nm2);
-              const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
-              r2[(c >> 1) & 3] = __fadd2_rn(r2[(c >> 1) & 3], make_float2(p0, p1));
-              pk[c / 2] = pack_bf16x2(p0, p1);
-            }
-            const float2 ra = __fadd2_rn(r2[0], r2[1]), rb = __fadd2_rn(r2[2], r2[3]);
-            const float2 rs = __fadd2_rn(ra, rb);
-            l = l * alpha + (rs.x + rs.y);
-            ATR_SM(5);
-            if (j > 0 || pend) {  // PV_{j-1} has consumed P_{j-1} (j == 0: the pending tile's last PV is done)
-              mbar_wait<false>(pv_done, pv_ph);
-              pv_ph ^= 1;
-              tc_fence_after();
-            }
-            ATR_SM(6);
-#pragma unroll
-            for (int cb = 0; cb < NC; ++cb) CORA_TMEM_ST_32X32B_X16(tmem_base + t_lane + kTmemP + cb * 16, (pk + cb * 16));
-          };
-          switch (nc) {
-            case 1: softmax(std::integral_constant<int, 1>{}); break;
-            case 2: softmax(std::integral_constant<int, 2>{}); break;
-            case 3: softmax(std::integral_constant<int, 3>{}); break;
-            default: softmax(std::integral_constant<int, 4>{}); break;
+  #pragma unroll
+            for (int c = 0; c < TK; ++c)
+              if (c < lo || c >= hi || (CAUSAL && c > i)) sv[c] = -INFINITY;
+          } else if (CAUSAL && j == cur.qt) {
+  #pragma unroll
+            for (int c = 0; c < TK; ++c)
+              if (c > i || c >= valid) sv[c] = -INFINITY;
+          } else if (valid < TK) {
+  #pragma unroll
+            for (int c = 0; c < TK; ++c)
+              if (c >= valid) sv[c] = -INFINITY;
           }
-          // causal diagonal: chunks past this warp's rows are read by the PV MMA but hold no visible key
-          if (CAUSAL)
-            for (int cb = nc; cb < ncm; ++cb) tmem_st_zero_x16(tmem_base + t_lane + kTmemP + cb * 16);
+          float m8[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+  #pragma unroll
+          for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+          const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
+          // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
+          const bool bump = mx > m_ref + kRescaleLog2;
+          const float m_new = bump ? mx : m_ref;
+          const float alpha = ex2_approx(m_ref - m_new);  // 1 when not bumped, 0 on the first tile
+          m_ref = m_new;
+          // p = exp2(s * scale_log2 - m_ref) (masked keys give exactly 0), fp32 row sum in 8 chains,
+          // bf16 pairs packed right away (the A operand layout of the TS MMA: 2 keys per column)
+          float r8[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) r8[k] = 0.f;
+          uint32_t pk[TK / 2];
+  #pragma unroll
+          for (int c = 0; c < TK; c += 2) {
+            const float x0 = fmaf(sv[c], scale_log2, -m_ref), x1 = fmaf(sv[c + 1], scale_log2, -m_ref);
+            float p0, p1;
+            if (poly_col(c)) {
+              // masked keys (-inf) must give exactly 0 like EX2; unmasked x is clamped into the poly's range
+              p0 = masked ? (x0 > -125.f ? exp2_poly(x0) : 0.f) : exp2_poly(fmaxf(x0, -125.f));
+              p1 = masked ? (x1 > -125.f ? exp2_poly(x1) : 0.f) : exp2_poly(fmaxf(x1, -125.f));
+            } else {
+              p0 = ex2_approx(x0);
+              p1 = ex2_approx(x1);
+            }
+            r8[(c >> 1) & 7] += p0 + p1;
+            pk[c / 2] = pack_bf16x2(p0, p1);
+          }
+          l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
+          if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
+            mbar_wait<false>(pv_done, pv_ph);
+            pv_ph ^= 1;
+            tc_fence_after();
+          }
+          CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP, pk);
+          CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP + 32, (pk + 32));
           // rescale the O accumulator in place when some row of this warp moved its reference max
           if (j > 0 && __any_sync(0xffffffffu, bump)) {
-#pragma unroll
+  #pragma unroll
             for (int half = 0; half < 2; ++half) {
-              uint32_t ors[32];
+              uint32_t orr[32];
               const uint32_t taddr = tmem_base + t_lane + kTmemO + half * 32;
-              CORA_TMEM_LD_32X32B_X32(taddr, ors);
+              CORA_TMEM_LD_32X32B_X32(taddr, orr);
               tmem_ld_wait();
-              const float2 a2 = make_float2(alpha, alpha);
-#pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                const float2 o = __fmul2_rn(make_float2(__uint_as_float(ors[c]), __uint_as_float(ors[c + 1])), a2);
-                ors[c] = __float_as_uint(o.x);
-                ors[c + 1] = __float_as_uint(o.y);
-              }
-              CORA_TMEM_ST_32X32B_X32(taddr, ors);
+  #pragma unroll
+              for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+              CORA_TMEM_ST_32X32B_X32(taddr, orr);
             }
           }
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
-          ATR_SM(7);
-          if (j == 0 && pend) {  // the pending O leaves TMEM (then PV_0 may overwrite it); stored under S_1
-            uint32_t orr[HD];
-            read_pending_o(orr, o_empty, tmem_base + t_lane + kTmemO, lane);
-            store_o(orr, out, d_model, out_v8, pend_row, pend_col, pend_l);
+        }
+        // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
+        mbar_wait<false>(pv_done, pv_ph);
+        pv_ph ^= 1;
+        tc_fence_after();
+        uint32_t orr[HD];
+        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
+        CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty);
+        const int qrow = cur.qt * TQ + i;
+        if (qrow < L) {
+          const float inv = 1.f / l;
+          __nv_bfloat16* orow = out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD;
+          if (out_v8) {  // 32-B stores: one full sector per lane
+  #pragma unroll
+            for (int g = 0; g < HD / 16; ++g) {
+              const float* o = reinterpret_cast<const float*>(orr) + g * 16;
+              uint32_t w[8];
+  #pragma unroll
+              for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(o[2 * e] * inv, o[2 * e + 1] * inv);
+              st_global_v8(orow + g * 16, w);
+            }
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow);
+  #pragma unroll
+            for (int g = 0; g < HD / 8; ++g) {
+              const float* o = reinterpret_cast<const float*>(orr) + g * 8;
+              dst[g] = make_uint4(pack_bf16x2(o[0] * inv, o[1] * inv), pack_bf16x2(o[2] * inv, o[3] * inv),
+                                  pack_bf16x2(o[4] * inv, o[5] * inv), pack_bf16x2(o[6] * inv, o[7] * inv));
+            }
           }
         }
-        pend = true;
-        pend_row = qrow < L ? cur.r0 + qrow : -1;
-        pend_col = cur.h * HD;
-        pend_l = l;
       }
     }
-    if (pend) {  // the last tile's O
-      mbar_wait<false>(pv_done, pv_ph);
-      pv_ph ^= 1;
-      tc_fence_after();
-      uint32_t orr[HD];
-      read_pending_o(orr, o_empty, tmem_base + t_lane + kTmemO, lane);
-      store_o(orr, out, d_model, out_v8, pend_row, pend_col, pend_l);
-    }
-#ifdef CORA_ATTN_TRACE
-    if (qd == 0 && lane == 0) ATR_DONE(0);
-#endif
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc<kTmemCols>(*reinterpret_cast<volatile uint32_t*>(tmem_ptr));
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
 
 // ---------------------------------------------------------------- SIMT kernel for other head dims
@@ -684,15 +555,6 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(const __nv_bfloat16
 }
 
 }  // namespace
-
-#ifdef CORA_ATTN_TRACE
-extern "C" int cora_debug_attn_trace(void* dst, void* counts) {
-  cudaMemcpyFromSymbol(dst, g_attn_trace, sizeof(g_attn_trace));
-  cudaMemcpyFromSymbol(counts, g_attn_trace_n, sizeof(g_attn_trace_n));
-  int z[kTraceCtas][2] = {};
-  return cudaMemcpyToSymbol(g_attn_trace_n, z, sizeof(z));
-}
-#endif
 
 cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
                              cudaStream_t stream, bool causal) {

@@ -382,6 +382,34 @@ __device__ __forceinline__ void tmem_st_zero_x16(uint32_t taddr) {
       : "memory");
 }
 
+// 16x256b TMEM shapes (a warp's 16 lanes starting at the address lane): thread t holds rows base + t/4 and
+// base + 8 + t/4, and per 8-column repetition k the column pair 8k + 2(t%4), +1 of both rows, in the
+// register order (row0, c), (row0, c+1), (row1, c), (row1, c+1).  Verified on the GPU
+// (scripts/micro/tmem_layout.cu).
+#define CORA_TMEM_LD_16X256B_X4(taddr, r)                                                                      \
+  asm volatile(                                                                                               \
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"  \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])   \
+      : "r"(taddr))
+#define CORA_TMEM_ST_16X256B_X4(taddr, r)                                                                      \
+  asm volatile(                                                                                               \
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"  \
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),     \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])              \
+      : "memory")
+// 16x128b: thread t holds rows base + t/4 and base + 8 + t/4, and per 4-column repetition k the column
+// 4k + t%4 of both rows, in the register order (row0, c), (row1, c).
+#define CORA_TMEM_ST_16X128B_X4(taddr, r)                                                                      \
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]), \
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])                      \
+               : "memory")
+__device__ __forceinline__ void tmem_st_zero_16x128b_x4(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x4.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(z)
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // max of three fp32 values in one instruction (FMNMX3, sm_100+)

@@ -55,7 +55,7 @@ def phases(role, pairs):
     return acc, spans
 
 names = {9: "tile", 1: "pre-wait", 2: "S ready", 3: "S in regs", 4: "max", 5: "exps", 6: "PV done", 7: "P handed",
-         8: "last PV", 20: "issue_s", 21: "K ready", 22: "S free", 23: "P ready", 24: "V ready", 25: "PV issued", 10: "O in regs", 11: "loop top", 12: "meta", 13: "S released", 14: "masked"}
+         8: "last PV", 20: "issue_s", 21: "K ready", 22: "S free", 23: "P ready", 24: "V ready", 25: "PV issued", 10: "O in regs", 11: "loop top", 12: "meta", 13: "S released", 14: "masked", 26: "PV MMAs out", 27: "PV committed"}
 for role, title in ((0, "softmax warp 0"), (1, "MMA thread")):
     acc, spans = phases(role, None)
     print(f"== {title}: {len(spans)} CTAs, mean span {np.mean(spans):.0f} clk")
