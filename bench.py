@@ -55,13 +55,59 @@ def kernel_work(name, T, S2, d, dff, heads=8):
         # MUFU-bound: one exp2 per useful score, H * sum L^2
         return "alu", float(heads) * S2, "exp"
     if name == "out_proj_gemm":
-        return "tensor", 2.0 * T * d * d, "flop"
+        # HBM-bound (AI 170 < ridge 249): reads O and the residual x, writes H1 (LayerNorm 1
+        # fused into its epilogue), reads W_o once -- 3 T d + d^2 bf16 values
+        return "hbm", 2.0 * (3.0 * T * d + d * d), "byte"
     if name == "ff1_gemm":
         return "tensor", 2.0 * T * d * dff, "flop"
     if name == "ff2_gemm":
         return "tensor", 2.0 * T * dff * d, "flop"
     # LayerNorm: read + write one bf16 row each, gamma/beta once
     return "hbm", 2.0 * T * d * 2 + 2 * d * 4, "byte"
+
+
+def measured_ex2_peak():
+    """Measured MUFU.EX2 rate of this GPU (scripts/micro/ex2_bench.cu, built by __graft_entry__.build()):
+    the best Gex2/s over its configurations, or None when the binary is missing."""
+    exe = os.path.join(ROOT, "scripts", "micro", "ex2_bench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+    except Exception:
+        return None
+    best = None
+    for line in out.splitlines():
+        try:
+            j = json.loads(line)
+        except ValueError:
+            continue
+        if j.get("bench") == "ex2" and j.get("gex2_per_s", 0) < 1e5:
+            if best is None or j["gex2_per_s"] > best["gex2_per_s"]:
+                best = j
+    return best
+
+
+def tile_waste(lay, heads):
+    """Masked-lane share of the attention work actually run (the analogue of the paper's partial-padding
+    overhead), from the DEVICE work list the prelude built: every item covers
+    32 * ceil(rows / 32) query rows (its live warps) times 128 keys per KV tile; the useful part is
+    sum over sequences of L^2 per head."""
+    tb = {k: v.cpu().numpy() for k, v in lay.tables().items()}
+    n = int(tb["n_tiles"][0])
+    words = tb["tiles"][:n].astype(np.int64)
+    seq = tb["tile_seq"][:2 * n].reshape(-1, 2)
+    computed = 0
+    for wd, (_ro, L) in zip(words, seq):
+        packed = wd < 0
+        qt = (wd >> 24) & 0x7F
+        rows = int(L) if packed else min(128, int(L) - 128 * int(qt))
+        nkv = 1 if packed else -(-int(L) // 128)
+        computed += 32 * (-(-rows // 32)) * 128 * nkv
+    L = tb["row_off"][1:].astype(np.int64) - tb["row_off"][:-1].astype(np.int64)
+    useful = heads * int((L * L).sum())
+    return {"useful_scores": useful, "computed_lanes": computed, "waste": 1.0 - useful / computed if computed else 0.0,
+            "work_items": n}
 
 
 def load_peaks():
@@ -204,8 +250,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-stack", action="store_true", help="skip the 6-layer stack measurement")
-    ap.add_argument("--gather", default="torch", choices=["torch", "cora"],
-                    help="N > 1 all-gather: torch.distributed broadcasts, or the library's cora_allgather_ragged")
+    ap.add_argument("--groups", type=int, default=4,
+                    help="N > 1 6-layer stack: groups per rank whose gather overlaps the next group's compute")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     args = ap.parse_args()
@@ -224,7 +270,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2110_10221_b200 as P
-    from paper_2110_10221_b200.dist import allgather_ragged, shard_rows
+    from paper_2110_10221_b200.dist import NcclComm, ShardedStack, shard_rows
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -234,20 +280,24 @@ def main():
     # ---------------------------------------------------------------- workload (synthetic, seeded)
     w = synth.encoder_weights(d, H, dff)
     x_all = synth.activations(int(lengths.sum()), d)
-    plan, tok_begin = shard_rows(list(lengths), d, dff, world)
+    T_all = int(lengths.sum())
+    # the library's plan: contiguous, FLOP-balanced, window-aligned sequence ranges and their packed rows
+    plan, row_begin = shard_rows(list(lengths), d, dff, world)
     b0, b1 = plan[rank], plan[rank + 1]
     loc_len = lengths[b0:b1]
     T_loc = int(loc_len.sum())
-    x_loc = x_all[tok_begin[rank]:tok_begin[rank + 1]]
+    r0, r1 = row_begin[rank], row_begin[rank + 1]
+    x_loc = x_all[r0:r1]
     params = P.EncoderParams.from_host(w, device=dev)
     layer = P.EncoderLayer(params)
-    layer_launches = layer.launches(T_loc)  # 5: GEMM + LayerNorm fused (d_model 512), else 7
+    layer_launches = layer.launches(T_loc) if T_loc else layer.launches(T_all)  # 5: GEMM + LN fused, else 7
     fused_ln = layer_launches == 5
     len_dev = torch.tensor(loc_len, dtype=torch.int32, device=dev)
-    x_dev = torch.tensor(x_loc, dtype=torch.float32).to(torch.bfloat16).to(dev) if T_loc else \
-        torch.empty(0, d, dtype=torch.bfloat16, device=dev)
-    y_dev = torch.empty(T_loc, d, dtype=torch.bfloat16, device=dev)
-    y_full = torch.empty(int(lengths.sum()), d, dtype=torch.bfloat16, device=dev) if world > 1 else y_dev
+    # every rank holds the whole [T, d] input and output; its own rows are contiguous views of them, so the
+    # gather lands in place (no copy)
+    x_full = torch.tensor(x_all, dtype=torch.float32).to(torch.bfloat16).to(dev)
+    y_full = torch.empty(T_all, d, dtype=torch.bfloat16, device=dev)
+    x_dev, y_dev = x_full[r0:r1], y_full[r0:r1]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -258,36 +308,25 @@ def main():
     def step(events=None, pre_event=None):
         if pre_event is not None:
             pre_event.record()
-        if events is None and len(loc_len) and T_loc:
+        if events is None and T_loc:
             # the timed step: prelude + layer in one call (cora_encoder_forward: QKV runs under the prelude)
             fwd(len_dev, T_loc, x_dev, out=y_dev)
             return fwd
         # the instrumented step: separate calls, events between the kernels
-        lay = P.layout_build(len_dev, T_loc, H, 512) if len(loc_len) else None
+        lay = P.layout_build(len_dev, T_loc, H, 512) if T_loc else None
         lay_holder["lay"] = lay
-        if lay is not None and T_loc:
+        if lay is not None:
             layer(x_dev, lay, out=y_dev, events=events)
         elif events is not None:
             for e in events:
                 e.record()
         return lay
 
-    lib_comm = None
-    if world > 1 and args.gather == "cora":
-        from paper_2110_10221_b200.dist import NcclComm
-        lib_comm = NcclComm(rank, world)
-    row_off_all = [0]
-    for L_ in lengths:
-        row_off_all.append(row_off_all[-1] + int(L_))
+    # N > 1: the library's own NCCL communicator and in-place ragged all-gather (cora_allgather_ragged)
+    lib_comm = NcclComm(rank, world) if world > 1 else None
 
     def gather():
-        # the final all-gather of the ragged outputs: eager NCCL broadcasts, outside the graph
-        if lib_comm is not None:
-            if tok_begin[rank + 1] > tok_begin[rank]:
-                y_full[tok_begin[rank]:tok_begin[rank + 1]].copy_(y_dev)
-            lib_comm.allgather_ragged(y_full, row_off_all, plan)
-        else:
-            allgather_ragged(y_full, y_dev, tok_begin, rank, world)
+        lib_comm.allgather_ragged(y_full, row_begin)
 
     # correctness gate on the benchmarked configuration (status word)
     lay = step()
@@ -307,7 +346,7 @@ def main():
         e.record()
     torch.cuda.synchronize()
     graph = graph_ev = None
-    if not args.no_graph:
+    if not args.no_graph and T_loc:
         # the step as ONE CUDA graph: prelude (a1) + the layer kernels, chained with programmatic
         # dependent launch.  graph_ev is the same step with event-record nodes between the kernels (for
         # the per-kernel breakdown; those nodes break the PDL overlap, so it is timed separately).
@@ -356,8 +395,10 @@ def main():
         # ---- the timed region: exactly K steps
         if graph is not None:
             step_ms = timed(graph.replay, args.steps)
-        else:
+        elif T_loc:
             step_ms = timed(lambda: step(kev, pre_ev), args.steps, read_kernel_events)
+        else:  # a rank with no sequences: nothing to launch, it only joins the barriers and the gather
+            step_ms = timed(lambda: None, args.steps)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -370,21 +411,22 @@ def main():
         kern_step_ms = step_ms
 
     ms_local = float(np.mean(step_ms))
-    kern_ms = {k: float(np.mean([rec[j] for rec in kern_rec])) for j, k in enumerate(KERNELS)}
-    prelude_ms = float(np.mean(pre_rec))
+    kern_ms = {k: float(np.mean([rec[j] for rec in kern_rec])) if kern_rec else 0.0 for j, k in enumerate(KERNELS)}
+    prelude_ms = float(np.mean(pre_rec)) if pre_rec else 0.0
+    pct_local = [float(np.percentile(step_ms, q)) for q in (10, 50, 90)]
     if world > 1:
-        t = torch.tensor([ms_local], device=dev)
+        t = torch.tensor([ms_local] + pct_local, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, *pct = (float(v) for v in t.tolist())
     else:
-        ms = ms_local
+        ms, pct = ms_local, pct_local
 
     # ---------------------------------------------------------------- N > 1: the all-gather
     # `value` is the compute makespan (max over ranks from a common barrier, the scaling
     # target); the NCCL all-gather of the ragged outputs is timed alone (ii) and with the step (iii)
     gather_info = None
     if world > 1:
-        run_step = graph.replay if graph is not None else (lambda: step())
+        run_step = graph.replay if graph is not None else ((lambda: step()) if T_loc else (lambda: None))
         for _ in range(args.warmup):
             gather()
         torch.cuda.synchronize()
@@ -400,68 +442,96 @@ def main():
         t = torch.tensor([g_ms, sg_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         g_ms, sg_ms = (float(v) for v in t.tolist())
-        gather_info = {"allgather_ms": g_ms, "bytes_received_per_rank": int((int(lengths.sum()) - T_loc) * d * 2),
+        gather_info = {"allgather_ms": g_ms, "bytes_received_per_rank": int((T_all - T_loc) * d * 2),
+                       "path": "cora_allgather_ragged (the library's NCCL communicator, grouped in-place broadcasts)",
                        "with_gather": {"ms_per_step": sg_ms,
                                        "value": useful_flops(lengths, d, dff) / (sg_ms * 1e-3) / 1e12,
                                        "unit": "TFLOP/s"},
-                       "note": "value / ms_per_step: compute makespan (prelude + layer per rank, max over ranks); "
-                               "the NCCL all-gather of the outputs runs after it (allgather_ms alone, with_gather "
-                               "end to end)"}
+                       "note": "value / ms_per_step: (i) compute makespan (prelude + layer per rank, max over "
+                               "ranks); (ii) allgather_ms: the gather alone; (iii) with_gather: the step then the "
+                               "gather, end to end; stack6: the 6-layer model with the gather overlapped"}
 
     # ---------------------------------------------------------------- the paper's 6-layer model (SURVEY f-4)
     # one layout (prelude) per batch shared by 6 layers, one CUDA graph per
     # step, L2 flushed between steps like the headline number; reported beside it, not instead of it
     stack = None
-    if not args.no_stack and T_loc and world == 1:
+    if not args.no_stack:
         stack_params = [P.EncoderParams.from_host(synth.encoder_weights(d, H, dff, seed=200 + i), device=dev)
                         for i in range(6)]
-        enc_stack = P.EncoderStack(stack_params)
-        y_stack = torch.empty_like(y_dev)
-
-        def stack_step():
-            enc_stack(x_dev, P.layout_build(len_dev, T_loc, H, 512), out=y_stack)
-
-        stack_step()
-        torch.cuda.synchronize()
-        g_stack = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_stack):
-            stack_step()
-        for _ in range(args.warmup):
-            g_stack.replay()
-        torch.cuda.synchronize()
         n_stack = max(3, min(args.steps, 50))
-        st_ms = float(np.mean(timed(g_stack.replay, n_stack)))
+        if world == 1:
+            enc_stack = P.EncoderStack(stack_params)
+            y_stack = torch.empty_like(y_dev)
+
+            def stack_step():
+                enc_stack(x_dev, P.layout_build(len_dev, T_loc, H, 512), out=y_stack)
+
+            stack_step()
+            torch.cuda.synchronize()
+            g_stack = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_stack):
+                stack_step()
+            for _ in range(args.warmup):
+                g_stack.replay()
+            torch.cuda.synchronize()
+            st_ms = float(np.mean(timed(g_stack.replay, n_stack)))
+            what = "prelude(a1) once + 6 encoder layers, one CUDA graph"
+        else:
+            # every rank: its sequences in `groups` window-aligned groups, each one layout through the 6
+            # layers; group g's rows are gathered (NCCL, side stream) while group g + 1 computes
+            sh = ShardedStack(stack_params, n_groups=args.groups)
+            len_all_dev = torch.tensor(lengths, dtype=torch.int32, device=dev)
+            len_all_host = torch.tensor(lengths, dtype=torch.int32)
+            y_sh = torch.empty_like(y_full)
+
+            def stack_step():
+                sh(len_all_dev, len_all_host, x_full, comm=lib_comm, out=y_sh)
+
+            for _ in range(args.warmup):
+                stack_step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            st_ms = float(np.mean(timed(stack_step, n_stack)))
+            t = torch.tensor([st_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            st_ms = float(t.item())
+            what = (f"cora_encoder_stack_sharded_fwd: per rank {args.groups} groups x (prelude + 6 layers), each "
+                    "group's outputs all-gathered while the next computes; every rank ends with all T rows")
         stack = {"layers": 6, "ms_per_step": st_ms, "steps": n_stack,
                  "value": 6 * useful_flops(lengths, d, dff) / (st_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                 "step": "prelude(a1) once + 6 encoder layers, one CUDA graph"}
+                 "step": what}
 
     # ---------------------------------------------------------------- e2e: host buffers through the C ABI
     e2e = None
-    if not args.no_e2e and T_loc:
-        hf = P.HostForward(params, len(loc_len), T_loc, 512, device=dev)
-        len_h = torch.tensor(loc_len, dtype=torch.int32).pin_memory()
-        x_h = torch.tensor(x_loc, dtype=torch.float32).to(torch.bfloat16).pin_memory()
-        y_h = torch.empty(T_loc, d, dtype=torch.bfloat16).pin_memory()
-        for _ in range(args.warmup):
-            hf(len_h, x_h, y_h)
-        torch.cuda.synchronize()
-        assert hf.status() == 0
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for i in range(args.steps):
-            if not args.no_flush:
-                flush.zero_()
-            ev[i][0].record(stream)
-            hf(len_h, x_h, y_h)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-        if world > 1:
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h = 0.0, 0, 0
+        if T_loc:
+            hf = P.HostForward(params, len(loc_len), T_loc, 512, device=dev)
+            len_h = torch.tensor(loc_len, dtype=torch.int32).pin_memory()
+            x_h = torch.tensor(x_loc, dtype=torch.float32).to(torch.bfloat16).pin_memory()
+            y_h = torch.empty(T_loc, d, dtype=torch.bfloat16).pin_memory()
+            for _ in range(args.warmup):
+                hf(len_h, x_h, y_h)
+            torch.cuda.synchronize()
+            assert hf.status() == 0
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            for i in range(args.steps):
+                if not args.no_flush:
+                    flush.zero_()
+                ev[i][0].record(stream)
+                hf(len_h, x_h, y_h)
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+            h2d, d2h = int(x_h.numel() * 2 + len_h.numel() * 4), int(y_h.numel() * 2)
+        if world > 1:  # every rank joins (an empty rank contributes 0), so none waits forever
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": useful_flops(lengths, d, dff) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(x_h.numel() * 2 + len_h.numel() * 4),
-               "d2h_bytes_per_step": int(y_h.numel() * 2), "path": "cora_encoder_forward_host (pinned host buffers)"}
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "cora_encoder_forward_host (pinned host buffers)"}
 
     if rank != 0:
         if world > 1:
@@ -469,6 +539,7 @@ def main():
         return
 
     peaks = load_peaks()
+    ex2 = measured_ex2_peak()
     total_flops = useful_flops(lengths, d, dff)
     value = total_flops / (ms * 1e-3) / 1e12
     T, S2 = int(loc_len.sum()), int((loc_len ** 2).sum())
@@ -488,12 +559,19 @@ def main():
             kernels[k] = {"ms": kern_ms[k], "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                           "frac": ach / peak}
         elif bound == "alu":
-            # exponentials: MUFU.EX2 16 / clk / SM (B200; 2x on B300 only) x SMs x max SM clock
+            # exponentials vs the MUFU.EX2 rate measured on this GPU (scripts/micro/ex2_bench.cu), else the
+            # nominal 16 / clk / SM x SMs x max SM clock (2x on B300 only)
             ach = work / dur / 1e9
-            peak = 16.0 * sm_count * (clocks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e9
+            if ex2 is not None:
+                peak = ex2["gex2_per_s"]
+                src = (f"measured: scripts/micro/ex2_bench.cu ({ex2['ex2_per_clk_per_sm_at_max_clock']:.2f} "
+                       "EX2/clk/SM at the max clock)")
+            else:
+                peak = 16.0 * sm_count * (clocks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e9
+                src = "nominal: 16 MUFU.EX2/clk/SM x SMs x max SM clock (ex2 microbenchmark missing)"
             tf = 4.0 * d * S2 / dur / 1e12
             kernels[k] = {"ms": kern_ms[k], "bound": "alu", "achieved": ach, "peak": peak, "unit": "Gexp/s",
-                          "frac": ach / peak, "peak_source": "16 MUFU.EX2/clk/SM x SMs x max SM clock (DESIGN.md)",
+                          "frac": ach / peak, "peak_source": src,
                           "tensor_view": {"achieved": tf, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                                           "frac": tf / peaks["bf16_tflops_sustained"]}}
         else:
@@ -501,6 +579,10 @@ def main():
             peak = peaks["hbm_gbs"]
             kernels[k] = {"ms": kern_ms[k], "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                           "frac": ach / peak}
+            if k == "out_proj_gemm":
+                tf = 2.0 * T * d * d / dur / 1e12
+                kernels[k]["tensor_view"] = {"achieved": tf, "peak": peaks["bf16_tflops_sustained"],
+                                             "unit": "TFLOP/s", "frac": tf / peaks["bf16_tflops_sustained"]}
     for k in ("out_proj_gemm", "ff2_gemm"):
         if fused_ln:
             kernels[k]["epilogue"] = "bias + residual + LayerNorm (fused)"
@@ -514,6 +596,8 @@ def main():
                 "traffic": traffic,
                 "peak_source": kernels[dom].get("peak_source") or (
                     peaks["source"] + (" sustained" if kernels[dom]["bound"] == "tensor" else ""))}
+
+    waste = tile_waste(P.layout_build(len_dev, T_loc, H, 512), H) if T_loc else None
 
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -545,7 +629,9 @@ def main():
                    "launch": "eager" if args.no_graph else "CUDA graph replay per step, programmatic dependent launch"},
         "frac_of_peak": {"burst": value / peaks["bf16_tflops"], "sustained": value / peaks["bf16_tflops_sustained"],
                          "source": peaks["source"]},
+        "ms_percentiles": {"p10": pct[0], "p50": pct[1], "p90": pct[2]},
         "padded_over_useful_flops": padded_flops(lengths, d, dff) / total_flops,
+        "attention_tile_waste": waste,
         "roofline": roofline,
         "kernels": kernels,
         "prelude_ms": prelude_ms,

@@ -86,6 +86,9 @@ typedef struct cora_layout {
   int32_t total_tokens; /* T = sum_b L_b (host-known: the caller packed X) */
   int32_t n_tiles_max;  /* host bound on the attention work list length */
   int32_t _pad;
+  int64_t total_attn;   /* host-visible S2 = sum_b L_b^2 (the ragged score tensor's size per head, A_1 of
+                           X[b,i,h,j]): -1 after cora_layout_build (the lengths live on the device), filled
+                           by cora_layout_status, which synchronises anyway */
   const int32_t* lengths; /* [B]   L_b (caller-owned) */
   int32_t* row_off;       /* [B+1] row_off[b] = sum_{j<b} L_j   (A_1 of [b,i,c], exclusive) */
   int64_t* attn_off;      /* [B+1] attn_off[b] = sum_{j<b} L_j^2 (A_1 of X[b,i,h,j]) */
@@ -135,8 +138,8 @@ size_t cora_layout_workspace_bytes(int32_t batch, int32_t total_tokens, int32_t 
 cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
                                 int32_t max_len, void* ws, size_t ws_bytes, cora_layout_t* out, void* stream);
 
-/* Synchronise `stream` and read the device status word: CORA_OK or CORA_ERR_DATA. */
-cora_status_t cora_layout_status(const cora_layout_t* layout, void* stream);
+/* Synchronise `stream`, read the device status word (CORA_OK or CORA_ERR_DATA) and fill layout->total_attn. */
+cora_status_t cora_layout_status(cora_layout_t* layout, void* stream);
 
 /* ---------------------------------------------------------------- whole layer */
 
@@ -234,10 +237,11 @@ cora_status_t cora_linear_fwd(const void* a, const void* w, const void* bias, co
 /* c[m, n] = LN(act(a w^T + bias) + residual; gamma, beta, eps) with the LayerNorm (post-LN, biased
  * variance, fp32 statistics of the bf16-rounded pre-LN values, readings
  * c2/c3) fused into the GEMM epilogue: a 4-CTA cluster (two CTA pairs) owns full rows and exchanges the
- * row statistics through distributed shared memory.  The fused kernel needs n == 512, m > 128 and
- * act == CORA_ACT_NONE; with an activation (n == 512, m > 128, or any n % 8 == 0) the call runs the
- * GEMM into a stream-ordered temporary (cudaMallocAsync) and then the LayerNorm kernel.  Other shapes
- * with act NONE return CORA_ERR_UNSUPPORTED; residual, gamma, beta non-NULL; bias may be NULL. */
+ * row statistics (mean, M2 pairs merged with Chan's formula: no E[v^2] - mean^2 cancellation) through
+ * distributed shared memory.  The fused kernel needs n == 512, m > 128 and act == CORA_ACT_NONE; other
+ * shapes with n % 8 == 0 (an activation, another n) run the GEMM with its epilogue into c and then the
+ * LayerNorm kernel in place on c (no temporary, no allocation).  n % 8 != 0: CORA_ERR_UNSUPPORTED;
+ * residual, gamma, beta non-NULL; bias may be NULL. */
 cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, const void* bias, const void* residual,
                                                  const float* gamma, const float* beta, float eps, void* c, int32_t m,
                                                  int32_t n, int32_t k, cora_act_t act, void* stream);
@@ -295,12 +299,28 @@ cora_status_t cora_trmm_fwd(const void* l, const void* b, void* c, int32_t n, in
 
 /* ---------------------------------------------------------------- multi-GPU (host logic) */
 
+/* Short-sequence windows (reading f4-r1) are built by the prelude for batches of at most this many sequences. */
+#define CORA_PACK_MAX_BATCH 1024
+
 /* Contiguous sequence partition over n_ranks minimising the max per-rank cost,
  * cost(L) = 2L(4d^2 + 2 d d_ff) + 4 d L^2 (the sequence's useful FLOPs; BASELINE.json
  * north_star "balanced on sum(L_i d + L_i^2) FLOPs"); canonical greedy-left among optimal
- * plans (reading s1).  seq_begin_host[0..n_ranks]: rank r owns [begin[r], begin[r+1]). */
+ * plans (reading s1).  A boundary never splits a short-sequence window of the batch (reading s2:
+ * batches of <= CORA_PACK_MAX_BATCH sequences), so every rank rebuilds the one-GPU windows of its
+ * sequences and the sharded result equals the one-GPU result row for row.  Host-only (no GPU needed).
+ * seq_begin_host[0..n_ranks]: rank r owns sequences [begin[r], begin[r+1]); row_begin_host[0..n_ranks]
+ * (may be NULL): the same ranges as packed token rows (the exclusive prefix of the lengths at begin[r]).
+ * CORA_ERR_INVALID on bad arguments (n_ranks < 1, batch < 0, a negative length, NULL pointers). */
 cora_status_t cora_shard_plan(const int32_t* lengths_host, int32_t batch, int32_t d_model, int32_t d_ff,
-                              int32_t n_ranks, int32_t* seq_begin_host);
+                              int32_t n_ranks, int32_t* seq_begin_host, int32_t* row_begin_host);
+
+/* Split every rank's range of a plan into n_groups contiguous groups of about equal token counts, cutting
+ * only where cora_shard_plan may cut (groups may be empty).  group_seq_host / group_row_host:
+ * [n_ranks][n_groups + 1] (row-major; group_row_host may be NULL): group g of rank r is sequences
+ * [gs[r][g], gs[r][g+1]) = rows [gr[r][g], gr[r][g+1]).  Deterministic: every rank derives the same groups
+ * (the schedule of cora_encoder_stack_sharded_fwd's overlapped gather).  Host-only. */
+cora_status_t cora_shard_groups(const int32_t* lengths_host, int32_t batch, const int32_t* seq_begin_host,
+                                int32_t n_ranks, int32_t n_groups, int32_t* group_seq_host, int32_t* group_row_host);
 
 /* The final all-gather of the sequence-sharded layer's ragged outputs over NCCL, resolved
  * at run time (dlopen of libnccl.so.2: the copy torch loaded when called from Python).  Bootstrap: rank 0
@@ -312,14 +332,34 @@ cora_status_t cora_comm_get_unique_id(void* id_out_host);
 cora_status_t cora_comm_init(void** comm, const void* nccl_unique_id_host, int32_t n_ranks, int32_t rank);
 cora_status_t cora_comm_destroy(void* comm);
 
-/* In-place variable-size all-gather of out[T, d] (dt = bf16 or fp32, device): rank r owns the rows of
- * sequences [seq_begin_host[r], seq_begin_host[r+1]) (cora_shard_plan), i.e. rows
- * [row_off_host[seq_begin_host[r]], row_off_host[seq_begin_host[r+1]]) (row_off_host: the batch's exclusive
- * token prefix, host, [batch + 1]); after the call every rank holds all T rows in the original order.
- * ncclGroupStart; one ncclBroadcast per rank with a non-empty range (root r); ncclGroupEnd -- enqueued on
- * `stream`.  Collective: every rank of the communicator calls it with the same tables. */
-cora_status_t cora_allgather_ragged(void* comm, const int32_t* row_off_host, const int32_t* seq_begin_host,
-                                    void* out, int32_t d, cora_dtype_t dt, void* stream);
+/* In-place variable-size all-gather of out[T, d] (dt = bf16 or fp32, device): rank r owns rows
+ * [row_begin_host[r], row_begin_host[r+1]) (cora_shard_plan's row_begin_host, [n_ranks + 1] of the
+ * communicator); after the call every rank holds all T rows in the original order.  ncclGroupStart; one
+ * ncclBroadcast per rank with a non-empty range (root r); ncclGroupEnd -- enqueued on `stream`.  A
+ * one-rank communicator is a no-op.  Collective: every rank of the communicator calls it with the same table. */
+cora_status_t cora_allgather_ragged(void* comm, const int32_t* row_begin_host, void* out, int32_t d, cora_dtype_t dt,
+                                    void* stream);
+
+/* Workspace for cora_encoder_stack_sharded_fwd: one layout (batch bound) + cora_encoder_stack_workspace_bytes. */
+size_t cora_encoder_stack_sharded_workspace_bytes(const cora_encoder_params_t* layers, int32_t n_layers, int32_t batch,
+                                                  int32_t total_tokens, int32_t max_len);
+
+/* The sequence-sharded encoder stack with its gather: every rank computes the layers
+ * of its sequences (cora_shard_plan from lengths_host, identical on every rank) and, at the end, holds all
+ * T output rows.  The rank's range is cut into n_groups window-aligned groups (cora_shard_groups); each
+ * group is ONE ragged batch through all n_layers layers on ONE layout (the prelude once per group, not per
+ * layer: PAPER.md:955-959), and as soon as group g is done its rows leave for every rank (one grouped set of
+ * in-place ncclBroadcasts per group, on a library-owned side stream) while group g + 1 computes -- the
+ * gather is amortised over the layers and overlapped with the compute.  lengths: device int32 [batch];
+ * lengths_host: the same on the host (sum must equal total_tokens); x, y: [T, d_model] bf16 device buffers
+ * indexed by packed row (only the rank's own rows of x are read; all of y is written), x != y.
+ * comm: a communicator (cora_comm_init) or NULL for one rank (no collective).  n_groups in [1, 16].
+ * The caller's stream waits for the side stream before the call returns its work (the call is asynchronous).
+ * Collective when comm has > 1 rank: every rank calls it with the same lengths_host / n_groups. */
+cora_status_t cora_encoder_stack_sharded_fwd(const cora_encoder_params_t* layers, int32_t n_layers,
+                                             const int32_t* lengths, const int32_t* lengths_host, int32_t batch,
+                                             int32_t total_tokens, int32_t max_len, void* comm, int32_t n_groups,
+                                             const void* x, void* y, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- misc */
 const char* cora_status_string(cora_status_t s);

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     linear_residual_layernorm,
     ragged_attention,
     ragged_softmax,
+    shard_groups,
     shard_plan,
     trmm,
     vgemm,

@@ -24,7 +24,8 @@ EXPORTS = (
     "cora_layout_workspace_bytes", "cora_layout_build", "cora_layout_status", "cora_encoder_workspace_bytes",
     "cora_encoder_layer_fwd", "cora_encoder_layer_fwd_ex", "cora_encoder_layer_launches", "cora_encoder_stack_workspace_bytes", "cora_encoder_stack_fwd", "cora_encoder_forward_workspace_bytes", "cora_encoder_forward", "cora_forward_host_workspace_bytes",
     "cora_encoder_forward_host", "cora_linear_fwd", "cora_linear_residual_layernorm_fwd", "cora_vgemm_workspace_bytes", "cora_vgemm_fwd", "cora_trmm_fwd", "cora_ragged_attention_fwd", "cora_ragged_masked_attention_fwd", "cora_ragged_softmax_fwd",
-    "cora_layernorm_fwd", "cora_shard_plan", "cora_comm_unique_id_bytes", "cora_comm_get_unique_id", "cora_comm_init", "cora_comm_destroy", "cora_allgather_ragged", "cora_status_string", "cora_device_sm_count", "cora_build_info",
+    "cora_layernorm_fwd", "cora_shard_plan", "cora_shard_groups", "cora_encoder_stack_sharded_workspace_bytes",
+    "cora_encoder_stack_sharded_fwd", "cora_comm_unique_id_bytes", "cora_comm_get_unique_id", "cora_comm_init", "cora_comm_destroy", "cora_allgather_ragged", "cora_status_string", "cora_device_sm_count", "cora_build_info",
 )
 
 
@@ -36,6 +37,7 @@ class Layout(ctypes.Structure):
         ("total_tokens", ctypes.c_int32),
         ("n_tiles_max", ctypes.c_int32),
         ("_pad", ctypes.c_int32),
+        ("total_attn", ctypes.c_int64),
         ("lengths", ctypes.c_void_p),
         ("row_off", ctypes.c_void_p),
         ("attn_off", ctypes.c_void_p),
@@ -102,13 +104,18 @@ def lib() -> ctypes.CDLL:
             "cora_ragged_masked_attention_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, f32, vp]),
             "cora_ragged_softmax_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, vp]),
             "cora_layernorm_fwd": (i32, [vp, vp, vp, vp, vp, i32, i32, f32, i32, vp]),
-            "cora_shard_plan": (i32, [ctypes.POINTER(ctypes.c_int32), i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32)]),
+            "cora_shard_plan": (i32, [ctypes.POINTER(ctypes.c_int32), i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int32),
+                                      ctypes.POINTER(ctypes.c_int32)]),
+            "cora_shard_groups": (i32, [ctypes.POINTER(ctypes.c_int32), i32, ctypes.POINTER(ctypes.c_int32), i32, i32,
+                                        ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+            "cora_encoder_stack_sharded_workspace_bytes": (sz, [ctypes.POINTER(EncoderParams), i32, i32, i32, i32]),
+            "cora_encoder_stack_sharded_fwd": (i32, [ctypes.POINTER(EncoderParams), i32, vp, ctypes.POINTER(ctypes.c_int32),
+                                                     i32, i32, i32, vp, i32, vp, vp, vp, sz, vp]),
             "cora_comm_unique_id_bytes": (i32, []),
             "cora_comm_get_unique_id": (i32, [vp]),
             "cora_comm_init": (i32, [ctypes.POINTER(ctypes.c_void_p), vp, i32, i32]),
             "cora_comm_destroy": (i32, [vp]),
-            "cora_allgather_ragged": (i32, [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), vp, i32,
-                                            i32, vp]),
+            "cora_allgather_ragged": (i32, [vp, ctypes.POINTER(ctypes.c_int32), vp, i32, i32, vp]),
             "cora_status_string": (ctypes.c_char_p, [i32]),
             "cora_device_sm_count": (i32, []),
             "cora_build_info": (ctypes.c_char_p, []),

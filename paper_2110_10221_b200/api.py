@@ -32,6 +32,24 @@ def _need_cuda(*ts):
             raise ValueError("libcora_b200 takes contiguous CUDA tensors only (no CPU fallback)")
 
 
+def _expect(t: Optional[torch.Tensor], shape, dtype, name: str, device=None, host: bool = False) -> None:
+    """Size / dtype / device check before a raw pointer crosses the C ABI (an undersized buffer would be
+    read or written out of range by the kernels or the copies)."""
+    if t is None:
+        return
+    if host:
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name}: contiguous host tensor required (pinned for asynchronous copies)")
+    elif not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name}: contiguous CUDA tensor required (no CPU fallback)")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+
+
 class RaggedLayout:
     """Device offset tables of one ragged batch (cora_layout_build).  Reused across layers."""
 
@@ -153,10 +171,9 @@ class EncoderLayer:
     def __call__(self, x: torch.Tensor, layout: RaggedLayout, out: Optional[torch.Tensor] = None,
                  stream=None, events: Optional[Sequence["torch.cuda.Event"]] = None) -> torch.Tensor:
         """events: optional C.LAYER_EVENTS torch.cuda.Event objects recorded around every kernel."""
-        _need_cuda(x)
         T = layout.total_tokens
-        if x.dtype != torch.bfloat16 or x.shape != (T, self.params.d_model):
-            raise ValueError("x must be bf16 [T, d_model]")
+        _expect(x, (T, self.params.d_model), torch.bfloat16, "x")
+        _expect(out, (T, self.params.d_model), torch.bfloat16, "out", x.device)
         nbytes = self.workspace_bytes(T)
         if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
             self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=x.device)
@@ -188,12 +205,10 @@ class EncoderForward:
 
     def __call__(self, lengths: torch.Tensor, total_tokens: int, x: torch.Tensor, out: Optional[torch.Tensor] = None,
                  stream=None) -> torch.Tensor:
-        _need_cuda(lengths, x, out)
-        if lengths.dtype != torch.int32:
-            raise ValueError("lengths must be int32")
         T, B = int(total_tokens), lengths.numel()
-        if x.dtype != torch.bfloat16 or x.shape != (T, self.params.d_model):
-            raise ValueError("x must be bf16 [T, d_model]")
+        _expect(lengths, (B,), torch.int32, "lengths")
+        _expect(x, (T, self.params.d_model), torch.bfloat16, "x", lengths.device)
+        _expect(out, (T, self.params.d_model), torch.bfloat16, "out", lengths.device)
         nbytes = int(C.lib().cora_encoder_forward_workspace_bytes(ctypes.byref(self.cp), B, T, self.max_len))
         if nbytes == 0:
             raise C.CoraError(C.CORA_ERR_INVALID, "cora_encoder_forward_workspace_bytes")
@@ -220,10 +235,9 @@ class EncoderStack:
 
     def __call__(self, x: torch.Tensor, layout: RaggedLayout, out: Optional[torch.Tensor] = None,
                  stream=None) -> torch.Tensor:
-        _need_cuda(x, out)
         T = layout.total_tokens
-        if x.dtype != torch.bfloat16 or x.shape != (T, self.params[0].d_model):
-            raise ValueError("x must be bf16 [T, d_model]")
+        _expect(x, (T, self.params[0].d_model), torch.bfloat16, "x")
+        _expect(out, (T, self.params[0].d_model), torch.bfloat16, "out", x.device)
         n = len(self.params)
         nbytes = int(C.lib().cora_encoder_stack_workspace_bytes(self.cps, n, T))
         if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
@@ -249,9 +263,12 @@ class HostForward:
         self.layout = C.Layout()
 
     def __call__(self, lengths_host: torch.Tensor, x_host: torch.Tensor, y_host: torch.Tensor, stream=None) -> None:
-        for t in (lengths_host, x_host, y_host):
-            if t.is_cuda or not t.is_contiguous():
-                raise ValueError("HostForward takes contiguous host tensors (pinned for async copies)")
+        d = self.params.d_model
+        _expect(lengths_host, (self.batch,), torch.int32, "lengths_host", host=True)
+        _expect(x_host, (self.total_tokens, d), torch.bfloat16, "x_host", host=True)
+        _expect(y_host, (self.total_tokens, d), torch.bfloat16, "y_host", host=True)
+        if int(lengths_host.sum()) != self.total_tokens:
+            raise ValueError("sum(lengths_host) != total_tokens")
         C.check(C.lib().cora_encoder_forward_host(ctypes.byref(self.cp), _ptr(lengths_host), self.batch,
                                                   self.total_tokens, self.max_len, _ptr(x_host), _ptr(y_host),
                                                   _ptr(self.ws), self.ws.numel(), ctypes.byref(self.layout),
@@ -267,9 +284,13 @@ def encoder_layer(x: torch.Tensor, layout: RaggedLayout, params: EncoderParams, 
 
 def linear(a: torch.Tensor, w: torch.Tensor, bias: Optional[torch.Tensor] = None,
            residual: Optional[torch.Tensor] = None, act: str = "none", out=None, stream=None) -> torch.Tensor:
-    _need_cuda(a, w, bias, residual)
     m, k = a.shape
     n = w.shape[0]
+    _expect(a, (m, k), torch.bfloat16, "a")
+    _expect(w, (n, k), torch.bfloat16, "w", a.device)
+    _expect(bias, (n,), torch.bfloat16, "bias", a.device)
+    _expect(residual, (m, n), torch.bfloat16, "residual", a.device)
+    _expect(out, (m, n), torch.bfloat16, "out", a.device)
     c = torch.empty(m, n, dtype=torch.bfloat16, device=a.device) if out is None else out
     C.check(C.lib().cora_linear_fwd(_ptr(a), _ptr(w), _ptr(bias), _ptr(residual), _ptr(c), m, n, k, _ACT[act],
                                     _stream(stream)), "cora_linear_fwd")
@@ -280,9 +301,15 @@ def linear_residual_layernorm(a: torch.Tensor, w: torch.Tensor, residual: torch.
                               beta: torch.Tensor, bias: Optional[torch.Tensor] = None, eps: float = 1e-5,
                               act: str = "none", out=None, stream=None) -> torch.Tensor:
     """c = LN(act(a w^T + bias) + residual) with the LayerNorm fused into the GEMM epilogue (n == 512)."""
-    _need_cuda(a, w, bias, residual, gamma, beta)
     m, k = a.shape
     n = w.shape[0]
+    _expect(a, (m, k), torch.bfloat16, "a")
+    _expect(w, (n, k), torch.bfloat16, "w", a.device)
+    _expect(bias, (n,), torch.bfloat16, "bias", a.device)
+    _expect(residual, (m, n), torch.bfloat16, "residual", a.device)
+    _expect(gamma, (n,), torch.float32, "gamma", a.device)
+    _expect(beta, (n,), torch.float32, "beta", a.device)
+    _expect(out, (m, n), torch.bfloat16, "out", a.device)
     c = torch.empty(m, n, dtype=torch.bfloat16, device=a.device) if out is None else out
     C.check(C.lib().cora_linear_residual_layernorm_fwd(_ptr(a), _ptr(w), _ptr(bias), _ptr(residual), _ptr(gamma),
                                                        _ptr(beta), eps, _ptr(c), m, n, k, _ACT[act], _stream(stream)),
@@ -300,6 +327,9 @@ def vgemm(a: torch.Tensor, b: torch.Tensor, dims, out: Optional[torch.Tensor] = 
     n_max = b.shape[2]
     if b.shape[:2] != (batch, k_max) or a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise ValueError("a [batch, M_max, K_max], b [batch, K_max, N_max], bf16")
+    if len(dims) != batch or any(len(row) != 3 for row in dims):
+        raise ValueError("dims: [batch][3] (M_i, N_i, K_i)")
+    _expect(out, (batch, m_max, n_max), torch.bfloat16, "out", a.device)
     dh = (ctypes.c_int32 * (3 * batch))(*[int(v) for row in dims for v in row])
     c = torch.zeros(batch, m_max, n_max, dtype=torch.bfloat16, device=a.device) if out is None else out
     nbytes = int(C.lib().cora_vgemm_workspace_bytes(batch, dh))
@@ -315,6 +345,7 @@ def trmm(l: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None, s
     n, n_cols = b.shape
     if l.shape != (n, n) or l.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise ValueError("l [n, n], b [n, n_cols], bf16")
+    _expect(out, (n, n_cols), torch.bfloat16, "out", b.device)
     c = torch.empty(n, n_cols, dtype=torch.bfloat16, device=b.device) if out is None else out
     C.check(C.lib().cora_trmm_fwd(_ptr(l), _ptr(b), _ptr(c), n, n_cols, _stream(stream)), "cora_trmm_fwd")
     return c
@@ -322,11 +353,10 @@ def trmm(l: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None, s
 
 def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, scale: Optional[float] = None,
                      out=None, stream=None, causal: bool = False) -> torch.Tensor:
-    _need_cuda(qkv)
     T = layout.total_tokens
     d = layout.heads * head_dim
-    if qkv.dtype != torch.bfloat16 or qkv.shape != (T, 3 * d):
-        raise ValueError("qkv must be bf16 [T, 3 * heads * head_dim]")
+    _expect(qkv, (T, 3 * d), torch.bfloat16, "qkv")
+    _expect(out, (T, d), torch.bfloat16, "out", qkv.device)
     o = torch.empty(T, d, dtype=torch.bfloat16, device=qkv.device) if out is None else out
     s = head_dim ** -0.5 if scale is None else scale
     fn = C.lib().cora_ragged_masked_attention_fwd if causal else C.lib().cora_ragged_attention_fwd
@@ -336,7 +366,13 @@ def ragged_attention(layout: RaggedLayout, qkv: torch.Tensor, head_dim: int, sca
 
 
 def ragged_softmax(layout: RaggedLayout, x: torch.Tensor, out=None, stream=None) -> torch.Tensor:
-    _need_cuda(x)
+    if x.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("x: bf16 or fp32")
+    if layout.c.total_attn < 0:
+        layout.status()  # once per layout: fills layout.c.total_attn (the size check needs S2 on the host)
+    n = layout.heads * int(layout.c.total_attn)
+    _expect(x, (n,), x.dtype, "x")
+    _expect(out, (n,), x.dtype, "out", x.device)
     dt = {torch.bfloat16: C.CORA_DT_BF16, torch.float32: C.CORA_DT_F32}[x.dtype]
     y = torch.empty_like(x) if out is None else out
     C.check(C.lib().cora_ragged_softmax_fwd(ctypes.byref(layout.c), _ptr(x), _ptr(y), dt, _stream(stream)),
@@ -346,21 +382,41 @@ def ragged_softmax(layout: RaggedLayout, x: torch.Tensor, out=None, stream=None)
 
 def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, residual: Optional[torch.Tensor] = None,
               eps: float = 1e-5, out=None, stream=None) -> torch.Tensor:
-    _need_cuda(x, gamma, beta, residual)
-    dt = {torch.bfloat16: C.CORA_DT_BF16, torch.float32: C.CORA_DT_F32}[x.dtype]
+    if x.dtype not in (torch.bfloat16, torch.float32) or x.dim() != 2:
+        raise ValueError("x: bf16 or fp32 [rows, cols]")
     rows, cols = x.shape
+    _expect(x, (rows, cols), x.dtype, "x")
+    _expect(residual, (rows, cols), x.dtype, "residual", x.device)
+    _expect(gamma, (cols,), torch.float32, "gamma", x.device)
+    _expect(beta, (cols,), torch.float32, "beta", x.device)
+    _expect(out, (rows, cols), x.dtype, "out", x.device)
+    dt = {torch.bfloat16: C.CORA_DT_BF16, torch.float32: C.CORA_DT_F32}[x.dtype]
     y = torch.empty_like(x) if out is None else out
     C.check(C.lib().cora_layernorm_fwd(_ptr(x), _ptr(residual), _ptr(gamma), _ptr(beta), _ptr(y), rows, cols, eps, dt,
                                        _stream(stream)), "cora_layernorm_fwd")
     return y
 
 
-def shard_plan(lengths: Sequence[int], d_model: int, d_ff: int, n_ranks: int) -> list:
+def shard_plan(lengths: Sequence[int], d_model: int, d_ff: int, n_ranks: int, rows: bool = False):
+    """cora_shard_plan: seq_begin[n_ranks + 1] (and row_begin[n_ranks + 1] with rows=True)."""
     B = len(lengths)
     arr = (ctypes.c_int32 * max(B, 1))(*[int(x) for x in lengths])
     out = (ctypes.c_int32 * (n_ranks + 1))()
-    C.check(C.lib().cora_shard_plan(arr, B, d_model, d_ff, n_ranks, out), "cora_shard_plan")
-    return list(out)
+    rb = (ctypes.c_int32 * (n_ranks + 1))()
+    C.check(C.lib().cora_shard_plan(arr, B, d_model, d_ff, n_ranks, out, rb), "cora_shard_plan")
+    return (list(out), list(rb)) if rows else list(out)
+
+
+def shard_groups(lengths: Sequence[int], seq_begin: Sequence[int], n_groups: int):
+    """cora_shard_groups: (group_seq, group_row), each [n_ranks][n_groups + 1] nested lists."""
+    B, R = len(lengths), len(seq_begin) - 1
+    arr = (ctypes.c_int32 * max(B, 1))(*[int(x) for x in lengths])
+    sb = (ctypes.c_int32 * (R + 1))(*[int(x) for x in seq_begin])
+    gs = (ctypes.c_int32 * (R * (n_groups + 1)))()
+    gr = (ctypes.c_int32 * (R * (n_groups + 1)))()
+    C.check(C.lib().cora_shard_groups(arr, B, sb, R, n_groups, gs, gr), "cora_shard_groups")
+    g = n_groups + 1
+    return [list(gs[r * g:(r + 1) * g]) for r in range(R)], [list(gr[r * g:(r + 1) * g]) for r in range(R)]
 
 
 def build_info() -> str:

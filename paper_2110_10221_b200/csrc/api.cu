@@ -178,6 +178,7 @@ cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t t
   L.max_len = max_len;
   L.total_tokens = total_tokens;
   L.n_tiles_max = static_cast<int32_t>(ntm);
+  L.total_attn = -1;  // known on the host after cora_layout_status
   L.lengths = lengths;
   L.row_off = reinterpret_cast<int32_t*>(w + c.row_off);
   L.attn_off = reinterpret_cast<int64_t*>(w + c.attn_off);
@@ -191,17 +192,21 @@ cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t t
   L.units = reinterpret_cast<int32_t*>(w + c.units);
   L.unit_seq = reinterpret_cast<int32_t*>(w + c.unit_seq);
   L.n_units = reinterpret_cast<int32_t*>(w + c.n_units);
-  launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream));
+  const cudaError_t e = launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream));
   *out = L;
-  return cuda_status(cudaGetLastError());
+  return e == cudaSuccess ? CORA_OK : CORA_ERR_CUDA;
 }
 
-cora_status_t cora_layout_status(const cora_layout_t* layout, void* stream) {
-  if (layout == nullptr || layout->status == nullptr) return CORA_ERR_INVALID;
+cora_status_t cora_layout_status(cora_layout_t* layout, void* stream) {
+  if (layout == nullptr || layout->status == nullptr || layout->attn_off == nullptr) return CORA_ERR_INVALID;
   int32_t st = 0;
+  int64_t s2 = 0;
   cudaError_t e = cudaMemcpyAsync(&st, layout->status, sizeof(st), cudaMemcpyDeviceToHost, as_stream(stream));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&s2, layout->attn_off + layout->batch, sizeof(s2), cudaMemcpyDeviceToHost, as_stream(stream));
   if (e == cudaSuccess) e = cudaStreamSynchronize(as_stream(stream));
   if (e != cudaSuccess) return CORA_ERR_CUDA;
+  layout->total_attn = st == 0 ? s2 : -1;
   return st == 0 ? CORA_OK : CORA_ERR_DATA;
 }
 
@@ -236,16 +241,13 @@ cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, c
   g.ln_beta = beta;
   g.ln_eps = eps;
   if (gemm_ln_supported(g)) return cuda_status(launch_gemm_ln(g, as_stream(stream)));
-  if (act == CORA_ACT_NONE || (n % 8) != 0) return CORA_ERR_UNSUPPORTED;
-  // with an activation: act(a w^T + bias) + residual into a stream-ordered temporary, then LayerNorm
+  if ((n % 8) != 0) return CORA_ERR_UNSUPPORTED;
+  // not fusable (an activation, or N != 512): act(a w^T + bias) + residual is written to c itself, then
+  // LayerNorm'd in place (each row is read completely before it is written) -- no temporary is allocated
   cudaStream_t s = as_stream(stream);
-  void* tmp = nullptr;
-  if (cudaMallocAsync(&tmp, static_cast<size_t>(m) * n * 2, s) != cudaSuccess) return CORA_ERR_CUDA;
-  g.c = tmp;
   cudaError_t e = launch_gemm(g, s);
-  if (e == cudaSuccess) e = launch_layernorm(tmp, nullptr, gamma, beta, c, m, n, eps, CORA_DT_BF16, s);
-  const cudaError_t f = cudaFreeAsync(tmp, s);
-  return cuda_status(e != cudaSuccess ? e : f);
+  if (e == cudaSuccess) e = launch_layernorm(c, nullptr, gamma, beta, c, m, n, eps, CORA_DT_BF16, s);
+  return cuda_status(e);
 }
 
 size_t cora_vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host) {
@@ -648,59 +650,6 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
   }
   if (cudaEventRecord(hp->done, hp->d2h) != cudaSuccess || cudaStreamWaitEvent(s, hp->done, 0) != cudaSuccess)
     return CORA_ERR_CUDA;
-  return CORA_OK;
-}
-
-cora_status_t cora_shard_plan(const int32_t* lengths_host, int32_t batch, int32_t d_model, int32_t d_ff,
-                              int32_t n_ranks, int32_t* seq_begin_host) {
-  if (n_ranks < 1 || batch < 0 || d_model <= 0 || d_ff <= 0 || seq_begin_host == nullptr ||
-      (batch > 0 && lengths_host == nullptr))
-    return CORA_ERR_INVALID;
-  // cost(L) = 2 L (4 d^2 + 2 d d_ff) + 4 d L^2  (useful FLOPs of one sequence)
-  const int64_t per_tok = 2ll * (4ll * d_model * d_model + 2ll * d_model * d_ff);
-  int64_t total = 0, hi_one = 0;
-  for (int32_t b = 0; b < batch; ++b) {
-    const int64_t L = lengths_host[b];
-    if (L < 0) return CORA_ERR_INVALID;
-    const int64_t cst = L * per_tok + 4ll * d_model * L * L;
-    total += cst;
-    if (cst > hi_one) hi_one = cst;
-  }
-  auto cost = [&](int32_t b) {
-    const int64_t L = lengths_host[b];
-    return L * per_tok + 4ll * d_model * L * L;
-  };
-  auto parts_needed = [&](int64_t cap) {
-    int32_t parts = 1;
-    int64_t run = 0;
-    for (int32_t b = 0; b < batch; ++b) {
-      const int64_t cb = cost(b);
-      if (run + cb > cap) {
-        ++parts;
-        run = 0;
-      }
-      run += cb;
-    }
-    return parts;
-  };
-  // smallest capacity C* with a greedy partition into <= n_ranks parts (greedy is optimal for a fixed cap)
-  int64_t lo = hi_one, hi = total > hi_one ? total : hi_one;
-  while (lo < hi) {
-    const int64_t mid = lo + (hi - lo) / 2;
-    if (parts_needed(mid) <= n_ranks)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  const int64_t cap = lo;
-  int32_t i = 0;
-  seq_begin_host[0] = 0;
-  for (int32_t r = 0; r < n_ranks - 1; ++r) {
-    int64_t run = 0;
-    while (i < batch && run + cost(i) <= cap) run += cost(i++);
-    seq_begin_host[r + 1] = i;
-  }
-  seq_begin_host[n_ranks] = batch;
   return CORA_OK;
 }
 

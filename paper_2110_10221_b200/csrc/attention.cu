@@ -564,13 +564,14 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
     CUtensorMap tm;
     if (!make_tmap_2d_bf16(&tm, qkv, 3ull * d, L.total_tokens, 3ull * d * 2, HD, TQ, true))
       return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!attr_set[dev]) {
       for (auto k : {attention_fwd_kernel<false>, attention_fwd_kernel<true>}) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem::kAlloc);
         if (e != cudaSuccess) return e;
       }
-      attr_set = true;
+      attr_set[dev] = true;
     }
     const int max_grid = 2 * device_sm_count();
     const int grid = L.n_tiles_max < max_grid ? L.n_tiles_max : max_grid;

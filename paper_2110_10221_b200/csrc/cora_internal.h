@@ -12,8 +12,13 @@ namespace cora {
 
 constexpr int kAttnHeadDim = 64;  // head_dim of the tcgen05 attention kernel
 
-void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
-                         const cora_layout_t& L, cudaStream_t stream);
+// Short-sequence windows (reading f4-r1) are built by the prelude for batches of at most this many sequences.
+#ifndef CORA_PACK_MAX_BATCH
+#define CORA_PACK_MAX_BATCH 1024
+#endif
+
+cudaError_t launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, const cora_layout_t& L, cudaStream_t stream);
 
 // GEMM: C[m,n] = act(A[m,k] B[n,k]^T + bias) + residual.  Tensor maps are built by the caller.
 struct GemmArgs {
@@ -53,6 +58,15 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint6
                        uint32_t box_inner, uint32_t box_outer, bool swizzle128);
 
 int device_sm_count();
+
+// Function attributes (max dynamic smem) and occupancy answers are per device: one-time setup state is
+// kept per device ordinal so one process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
 
 // Launch with programmatic dependent launch (PDL) enabled, and an optional cluster dimension.
 template <typename... KArgs, typename... Args>

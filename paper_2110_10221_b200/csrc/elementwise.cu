@@ -61,13 +61,15 @@ struct Vec<__nv_bfloat16> {
   }
 };
 
+// LayerNorm kernels may run in place (y == x): every row is read completely by the warp that writes it.
+//
 // Persistent warps; NV 16-byte vectors per lane held in registers (cols <= 32 * NV * E).  gamma and
 // beta are staged once per block in shared memory; each warp streams RPW rows per iteration with
 // all loads issued before the reductions (memory-level parallelism for an HBM-bound kernel).
 template <typename T, int NV, int RPW>
-__global__ void __launch_bounds__(256, 4) layernorm_kernel(const T* __restrict__ x, const T* __restrict__ res,
+__global__ void __launch_bounds__(256, 4) layernorm_kernel(const T* x, const T* __restrict__ res,
                                                            const float* __restrict__ gamma,
-                                                           const float* __restrict__ beta, T* __restrict__ y,
+                                                           const float* __restrict__ beta, T* y,
                                                            int32_t rows, int32_t cols, float eps) {
   constexpr int E = Vec<T>::E;
   // gamma/beta staged lane-major: element e of lane l's j-th vector at [(j*E + e)*32 + l], so a
@@ -160,8 +162,8 @@ constexpr int kLnConsumers = 8;
 
 template <typename T, int NV, int RPW>
 __global__ void __launch_bounds__(32 * (kLnConsumers + 1), 2)
-    layernorm_bulk_kernel(const T* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
-                          T* __restrict__ y, int32_t rows, int32_t cols, int32_t rc, float eps) {
+    layernorm_bulk_kernel(const T* x, const float* __restrict__ gamma, const float* __restrict__ beta,
+                          T* y, int32_t rows, int32_t cols, int32_t rc, float eps) {
   constexpr int E = Vec<T>::E;
   extern __shared__ __align__(128) uint8_t ln_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(ln_smem + kLnStages * kLnChunkBytes);
@@ -279,9 +281,9 @@ __global__ void __launch_bounds__(32 * (kLnConsumers + 1), 2)
 
 // Rows wider than the register budget: three passes over global memory (L1/L2 hits after the first).
 template <typename T>
-__global__ void __launch_bounds__(256) layernorm_wide_kernel(const T* __restrict__ x, const T* __restrict__ res,
+__global__ void __launch_bounds__(256) layernorm_wide_kernel(const T* x, const T* __restrict__ res,
                                                              const float* __restrict__ gamma,
-                                                             const float* __restrict__ beta, T* __restrict__ y,
+                                                             const float* __restrict__ beta, T* y,
                                                              int32_t rows, int32_t cols, float eps) {
   constexpr int E = Vec<T>::E;
   const int lane = threadIdx.x & 31;
@@ -330,12 +332,13 @@ cudaError_t launch_layernorm_bulk(const T* x, const float* g, const float* b, T*
   int rc = kLnChunkBytes / row_bytes;  // rows per chunk
   if (rc > 64) rc = 64;
   const size_t smem = kLnStages * kLnChunkBytes + 2 * kLnStages * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(layernorm_bulk_kernel<T, NV, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const int chunks = (rows + rc - 1) / rc;
   const int cap = 2 * device_sm_count();

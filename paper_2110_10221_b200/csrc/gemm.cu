@@ -103,6 +103,22 @@ struct GemmSmem {
   static_assert(kBytes <= 232448, "shared memory budget");
 };
 
+// LayerNorm row statistics of the fused epilogues as (mean, M2 = sum (v - mean)^2) pairs, merged across
+// column segments and CTAs with the pairwise formula of Chan et al.: no E[v^2] - mean^2 cancellation, so
+// rows whose |mean| is large against their spread keep an accurate variance.
+// Segment of n values with shifted sums s1 = sum (v - K), s2 = sum (v - K)^2:
+__device__ __forceinline__ float2 seg_moments(float K, float s1, float s2, float n) {
+  return make_float2(K + s1 / n, fmaxf(s2 - s1 * (s1 / n), 0.f));
+}
+// Merge a (na = k * n values) with b (n values); k = 1 (equal halves) by default.  For k = 1 the result is
+// symmetric in a and b (both CTAs of a row compute bitwise the same statistics).
+__device__ __forceinline__ float2 merge_moments(float2 a, float2 b, float n, int k = 1) {
+  const float na = n * static_cast<float>(k), nc = na + n;
+  const float d = b.x - a.x;
+  if (k == 1) return make_float2((a.x + b.x) * 0.5f, (a.y + b.y) + d * d * (n * 0.5f));
+  return make_float2(a.x + d * (n / nc), (a.y + b.y) + d * d * (na * n / nc));
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
@@ -364,7 +380,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 2) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
-      float s1 = 0.f, s2 = 0.f;
+      // shifted sums (shift K = the segment's first value): no cancellation when |mean| >> sigma
+      float s1 = 0.f, s2 = 0.f, K = 0.f;
 #pragma unroll
       for (int c = 0; c < kSeg / BK; ++c) {
         uint32_t r[64];
@@ -387,23 +404,23 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
           const uint32_t o = pack_bf16x2(v0 + bf16_lo(rw), v1 + bf16_hi(rw));
           vv[c * 32 + p2] = o;
           const float y0 = bf16_lo(o), y1 = bf16_hi(o);  // statistics of the rounded values
-          s1 += y0 + y1;
-          s2 = fmaf(y0, y0, fmaf(y1, y1, s2));
+          if (c == 0 && p2 == 0) K = y0;
+          const float d0 = y0 - K, d1 = y1 - K;
+          s1 += d0 + d1;
+          s2 = fmaf(d0, d0, fmaf(d1, d1, s2));
         }
       }
       float2* pa = part + acc * 2 * BM;
-      pa[hf * BM + row] = make_float2(s1, s2);
+      pa[hf * BM + row] = seg_moments(K, s1, s2, static_cast<float>(kSeg));
       named_bar_sync(1, 32 * EW);  // both column quarters of every row are in `part`
-      const float2 p0 = pa[row], p1 = pa[BM + row];
-      const float c1 = p0.x + p1.x, c2 = p0.y + p1.y;  // this CTA's 256-column partial
+      const float2 cm = merge_moments(pa[row], pa[BM + row], static_cast<float>(kSeg));  // this CTA's 256 columns
       if (hf == 0)
-        st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
+        st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, cm.x, cm.y, xch_remote0 + acc * 8);
       mbar_wait(&xch_bar[acc], acc_phase);
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(7);
-      const float2 pr = recv[acc * BM + row];
-      const float mean = (c1 + pr.x) * inv_n;
-      const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
-      const float rstd = rsqrtf(var + ln_eps);
+      const float2 rm = merge_moments(cm, recv[acc * BM + row], static_cast<float>(N / 2));
+      const float mean = rm.x;
+      const float rstd = rsqrtf(rm.y * inv_n + ln_eps);
       // straight from registers to the row in global memory (16-B stores; no staging buffer, whose 32 KB
       // hold a sixth pipeline stage instead)
       __nv_bfloat16* dst = out_ptr + static_cast<size_t>(grow) * N + nw;
@@ -487,7 +504,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 2) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
-      float s1 = 0.f, s2 = 0.f;
+      // shifted sums (shift K = the segment's first value): no cancellation when |mean| >> sigma
+      float s1 = 0.f, s2 = 0.f, K = 0.f;
 #pragma unroll 1
       for (int c = 0; c < S::kBufs; ++c) {
         uint32_t r[64];
@@ -516,30 +534,27 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
             const float v1 = __uint_as_float(r[ch * 8 + 2 * i + 1]) + bf16_hi(b2);
             o[i] = pack_bf16x2(v0 + bf16_lo(w[i]), v1 + bf16_hi(w[i]));
             const float y0 = bf16_lo(o[i]), y1 = bf16_hi(o[i]);  // statistics of the rounded values
-            s1 += y0 + y1;
-            s2 = fmaf(y0, y0, fmaf(y1, y1, s2));
+            if (ch == 0 && i == 0 && c == 0) K = y0;
+            const float d0 = y0 - K, d1 = y1 - K;
+            s1 += d0 + d1;
+            s2 = fmaf(d0, d0, fmaf(d1, d1, s2));
           }
           st_shared_v4(sbase + sw128_offset(lane, ch), o[0], o[1], o[2], o[3]);
         }
       }
       float2* pa = part + acc * (EW / 4) * BM;
-      pa[hf * BM + row] = make_float2(s1, s2);
+      pa[hf * BM + row] = seg_moments(K, s1, s2, static_cast<float>(S::kWarpCols));
       named_bar_sync(1, 32 * EW);  // every column group of every row is in `part`
-      float c1 = 0.f, c2 = 0.f;    // this CTA's 256-column partial
+      float2 cm = pa[row];         // this CTA's 256-column (mean, M2)
 #pragma unroll
-      for (int g = 0; g < EW / 4; ++g) {
-        const float2 pg = pa[g * BM + row];
-        c1 += pg.x;
-        c2 += pg.y;
-      }
+      for (int g = 1; g < EW / 4; ++g) cm = merge_moments(cm, pa[g * BM + row], static_cast<float>(S::kWarpCols), g);
       if (hf == 0)
-        st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, c1, c2, xch_remote0 + acc * 8);
+        st_async_v2f32(recv_remote0 + (acc * BM + row) * 8, cm.x, cm.y, xch_remote0 + acc * 8);
       mbar_wait(&xch_bar[acc], acc_phase);
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(7);
-      const float2 pr = recv[acc * BM + row];
-      const float mean = (c1 + pr.x) * inv_n;
-      const float var = fmaxf((c2 + pr.y) * inv_n - mean * mean, 0.f);
-      const float rstd = rsqrtf(var + ln_eps);
+      const float2 rm = merge_moments(cm, recv[acc * BM + row], static_cast<float>(N / 2));
+      const float mean = rm.x;
+      const float rstd = rsqrtf(rm.y * inv_n + ln_eps);
 #pragma unroll 1
       for (int c = 0; c < S::kBufs; ++c) {
         uint8_t* buf = cbuf + c * kEpiBufBytes;
@@ -712,17 +727,19 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
     tr = tc;  // unused
   }
   auto kern = gemm_bf16_tn_kernel<BN, STAGES, RESIDUAL, CL, LN, LNREG, ACT>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kAlloc);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const int m_blocks = (g.m + BM - 1) / BM, n_blocks = (g.n + BN - 1) / BN;
   const int units = ((m_blocks + (CL > 1 ? 1 : 0)) / (CL > 1 ? 2 : 1)) * (LN ? 1 : n_blocks);
   // persistent grid = the clusters that can be co-resident (clusters of 4 cannot use every SM: GPC
   // boundaries strand some), so no cluster waits for a second wave
-  static int max_clusters = 0;
+  static int max_clusters_dev[kMaxDevices] = {};
+  int& max_clusters = max_clusters_dev[dev];
   if (max_clusters == 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * (device_sm_count() / CL));

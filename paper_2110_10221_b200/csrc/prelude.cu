@@ -21,9 +21,6 @@ namespace {
 
 constexpr int kScanThreads = 1024;
 constexpr int kMaxBuckets = 129;  // ceil(16383/128) + 1 distinct q-tile counts
-#ifndef CORA_PACK_MAX_BATCH
-#define CORA_PACK_MAX_BATCH 1024
-#endif
 constexpr int kPackMaxBatch = CORA_PACK_MAX_BATCH;  // short-sequence windows (merged prelude, batch <= this)
 
 template <typename T>
@@ -372,8 +369,8 @@ __global__ void fusion_maps_kernel(const int32_t* __restrict__ row_off, const in
 
 }  // namespace
 
-void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads, int32_t max_len,
-                         const cora_layout_t& L, cudaStream_t stream) {
+cudaError_t launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, const cora_layout_t& L, cudaStream_t stream) {
   // one CTA of the scan sized to the batch (>= 1 warp, <= 1024 threads; larger batches loop in chunks)
   int threads = ((batch + 31) / 32) * 32;
   threads = threads < 32 ? 32 : (threads > kScanThreads ? kScanThreads : threads);
@@ -382,17 +379,17 @@ void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_to
     int blocks = (batch + kSeqPerBlock - 1) / kSeqPerBlock;
     if (blocks > device_sm_count()) blocks = device_sm_count();
     if (blocks < 1) blocks = 1;
-    static bool attr_set = false;  // static (~36 KB) + dynamic (up to 32 KB) smem exceeds the 48 KB default
-    if (!attr_set) {
-      if (cudaFuncSetAttribute(layout_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               sizeof(int32_t) * (kMergedMaxBatch + 1)) != cudaSuccess)
-        return;
-      attr_set = true;
+    static bool attr_set[kMaxDevices] = {};  // static (~36 KB) + dynamic (up to 32 KB) smem exceeds the 48 KB default
+    const int dev = current_device();
+    if (!attr_set[dev]) {
+      const cudaError_t e = cudaFuncSetAttribute(layout_merged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 sizeof(int32_t) * (kMergedMaxBatch + 1));
+      if (e != cudaSuccess) return e;
+      attr_set[dev] = true;
     }
-    launch_pdl(layout_merged_kernel, dim3(blocks), dim3(threads), sizeof(int32_t) * (batch + 1), stream, 1,
+    return launch_pdl(layout_merged_kernel, dim3(blocks), dim3(threads), sizeof(int32_t) * (batch + 1), stream, 1,
                lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off, L.tiles, L.tile_seq, L.n_tiles,
                L.units, L.unit_seq, L.n_units, L.status, L.seq_of_tok, L.pos_in_seq);
-    return;
   }
   layout_scan_kernel<<<1, threads, 0, stream>>>(lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off,
                                                 L.tiles, L.tile_seq, L.n_tiles, L.units, L.unit_seq, L.n_units,
@@ -402,6 +399,7 @@ void launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_to
     fusion_maps_kernel<<<(total_tokens + mt - 1) / mt, mt, 0, stream>>>(L.row_off, L.status, batch, total_tokens,
                                                                          L.seq_of_tok, L.pos_in_seq);
   }
+  return cudaGetLastError();
 }
 
 }  // namespace cora

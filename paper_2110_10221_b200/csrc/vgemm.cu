@@ -208,6 +208,10 @@ __global__ void __launch_bounds__(kVThreads, 1)
         uint32_t r[32];
         CORA_TMEM_LD_32X32B_X32(tmem_base + ((q * 32) << 16) + acc * VN + cb * 32, r);
         tmem_ld_wait();
+        if (w.kb == 0) {  // K_i == 0: no MMA ran for this unit, the accumulator holds stale data; C_i = 0
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = 0u;
+        }
         const int col0 = w.n0 + cb * 32;
         if (row < pm && col0 < pn && c_v8 && col0 + 32 <= pn) {
           // 32-B stores: one full sector per lane
@@ -247,10 +251,11 @@ __global__ void __launch_bounds__(kVThreads, 1)
 
 template <bool TRMM>
 cudaError_t set_smem_attr() {
-  static bool done = false;
-  if (done) return cudaSuccess;
+  static bool done[kMaxDevices] = {};
+  const int dev = current_device();
+  if (done[dev]) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(vgemm_kernel<TRMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-  if (e == cudaSuccess) done = true;
+  if (e == cudaSuccess) done[dev] = true;
   return e;
 }
 

@@ -53,19 +53,65 @@ def test_argument_validation_without_device():
     assert L.cora_status_string(2) == b"data error (bad lengths or sum(L) != T)"
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(12))
 def test_shard_plan_matches_oracle(seed):
     import paper_2110_10221_b200 as P
     rng = np.random.default_rng(seed)
     B = int(rng.integers(0, 40))
     R = int(rng.integers(1, 9))
-    L = [int(x) for x in rng.integers(0, 513, size=B)]
-    assert P.shard_plan(L, 512, 2048, R) == oracle.shard_plan(L, 512, 2048, R)
+    # mixes of long sequences and short ones that form windows (reading s2)
+    pool = [0, 1, 5, 30, 64, 100, 128, 129, 300, 512] if seed % 2 else list(range(0, 513))
+    L = [int(x) for x in rng.choice(pool, size=B)]
+    plan, rows = P.shard_plan(L, 512, 2048, R, rows=True)
+    assert plan == oracle.shard_plan(L, 512, 2048, R)
+    ro = oracle.row_offsets(L)
+    assert rows == [ro[b] for b in plan]
 
 
-def test_shard_plan_c4():
+@pytest.mark.parametrize("cfg", ["C4-wiki512", "C4-race", "mnli-128", "cola-32", "C5-skewed-128"])
+def test_shard_plan_paper_configs(cfg):
     import paper_2110_10221_b200 as P
     import synth
-    L = [int(x) for x in synth.config("C4-wiki512")[0]]
+    L = [int(x) for x in synth.config(cfg)[0]]
     for R in (1, 2, 4, 8):
         assert P.shard_plan(L, 512, 2048, R) == oracle.shard_plan(L, 512, 2048, R)
+
+
+def test_shard_plan_unconstrained_above_pack_limit():
+    import paper_2110_10221_b200 as P
+    L = [5] * 1100  # > CORA_PACK_MAX_BATCH: no windows, any cut is allowed
+    plan = P.shard_plan(L, 512, 2048, 4)
+    assert plan == [0, 275, 550, 825, 1100] == oracle.shard_plan(L, 512, 2048, 4)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5])
+def test_shard_groups_partition_window_aligned(G):
+    import paper_2110_10221_b200 as P
+    import synth
+    L = [int(x) for x in synth.config("mnli-128")[0]] + [300, 2, 3, 200]
+    ok = oracle.shard.allowed_cuts(L)
+    ro = oracle.row_offsets(L)
+    for R in (1, 2, 3):
+        plan = P.shard_plan(L, 512, 2048, R)
+        gseq, grow = P.shard_groups(L, plan, G)
+        for r in range(R):
+            assert gseq[r][0] == plan[r] and gseq[r][G] == plan[r + 1] and gseq[r] == sorted(gseq[r])
+            assert all(ok[c] for c in gseq[r])
+            assert grow[r] == [ro[b] for b in gseq[r]]
+
+
+def test_shard_entry_points_validate():
+    from paper_2110_10221_b200 import _lib as C
+    L = C.lib()
+    lens = (ctypes.c_int32 * 3)(3, -1, 4)
+    out = (ctypes.c_int32 * 3)()
+    assert L.cora_shard_plan(lens, 3, 512, 2048, 2, out, None) == C.CORA_ERR_INVALID  # negative length
+    assert L.cora_shard_plan(lens, 3, 512, 2048, 0, out, None) == C.CORA_ERR_INVALID  # no rank
+    sb = (ctypes.c_int32 * 3)(0, 2, 1)
+    gs = (ctypes.c_int32 * 8)()
+    good = (ctypes.c_int32 * 3)(3, 1, 4)
+    assert L.cora_shard_groups(good, 3, sb, 2, 3, gs, None) == C.CORA_ERR_INVALID  # decreasing plan
+    p = C.EncoderParams()
+    p.d_model, p.heads, p.d_ff = 512, 8, 2048
+    assert L.cora_encoder_stack_sharded_workspace_bytes(ctypes.byref(p), 0, 4, 16, 512) == 0
+    assert L.cora_encoder_stack_sharded_workspace_bytes(ctypes.byref(p), 2, 4, 16, 512) > 0

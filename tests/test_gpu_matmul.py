@@ -20,6 +20,7 @@ VGEMM_CASES = [
     [(512, 640, 512), (1408, 512, 1408), (640, 1408, 768)],  # the paper's range, ragged N tiles
     [(100, 72, 128), (1, 8, 64), (0, 16, 64), (257, 264, 192), (33, 0, 64)],  # M/N tails, empty problems
     [(300, 200, 200)],                                   # K tail == K_max (TMA zero-fill)
+    [(64, 64, 0), (128, 256, 64), (200, 100, 0)],        # K_i == 0: C_i = 0 (no stale accumulator)
 ]
 
 

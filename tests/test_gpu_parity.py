@@ -212,6 +212,45 @@ def test_linear_residual_layernorm_fused(m, k, use_bias):
     assert rel_err(to_np(c), ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("k", [512, 2048])  # the staged-residual (K < 1024) and register (K >= 1024) LN epilogues
+def test_linear_residual_layernorm_large_mean_rows(k):
+    """Rows whose |mean| / sigma is >= 100 (reading c3: biased variance).  The pre-LN
+    values must be exact in bf16 for the comparison to test the statistics and not the storage rounding
+    (reading c13), so a = 0 (the GEMM contributes exactly 0), no bias, and each residual row is
+    2^e (1 + j 2^-7), j in {-1, 0, 1}: one bf16 ulp of spread around a power of two (|mean| / sigma ~ 180).
+    A one-pass E[v^2] - mean^2 in fp32 loses the variance to cancellation here; the oracle is exact."""
+    m, n = 300, 512
+    rng = np.random.default_rng(61)
+    e = rng.integers(4, 14, size=(m, 1)).astype(np.float64)
+    j = rng.integers(-1, 2, size=(m, n)).astype(np.float64)
+    j[:, 0], j[:, 1] = -1.0, 1.0  # every row has a spread
+    r = (2.0 ** e) * (1.0 + j / 128.0)
+    r[::7] = synth.round_bf16(synth.normal((len(r[::7]), n), 62))  # ordinary rows mixed in
+    assert np.array_equal(synth.round_bf16(r), r)
+    a = np.zeros((m, k))
+    w = synth.round_bf16(synth.normal((n, k), 63) / math.sqrt(k))
+    g = synth.round_f32(1 + 0.1 * synth.normal((n,), 64))
+    be = synth.round_f32(0.1 * synth.normal((n,), 65))
+    c = P().linear_residual_layernorm(bf16_cuda(a), bf16_cuda(w), bf16_cuda(r), f32_cuda(g), f32_cuda(be))
+    ref = oracle.layernorm(r, g, be)
+    big = np.abs(r.mean(1)) / r.std(1) >= 100
+    assert big.sum() > m // 2
+    assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
+def test_linear_residual_layernorm_unfused_no_activation():
+    # n != 512: GEMM + residual into the output, then LayerNorm in place (no temporary allocation)
+    m, k, n = 300, 512, 256
+    a = synth.round_bf16(synth.normal((m, k), 66))
+    w = synth.round_bf16(synth.normal((n, k), 67) / math.sqrt(k))
+    r = synth.round_bf16(synth.normal((m, n), 68))
+    g = synth.round_f32(1 + 0.1 * synth.normal((n,), 69))
+    be = synth.round_f32(0.1 * synth.normal((n,), 70))
+    c = P().linear_residual_layernorm(bf16_cuda(a), bf16_cuda(w), bf16_cuda(r), f32_cuda(g), f32_cuda(be))
+    ref = oracle.layernorm(oracle.linear(a, w, None, residual=r), g, be)
+    assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
 @pytest.mark.parametrize("act", ["relu", "gelu"])
 def test_linear_residual_layernorm_with_activation(act):
     # activations take the two-launch path (GEMM + activation + residual, then LayerNorm)
@@ -264,10 +303,11 @@ def test_attention_16b_aligned_output():
 
 
 def test_linear_residual_layernorm_unsupported_shape():
+    # n % 8 != 0: rows of the output are not 16-B multiples (CORA_ERR_UNSUPPORTED)
     a = bf16_cuda(synth.normal((300, 64), 1))
-    w = bf16_cuda(synth.normal((256, 64), 2))
-    r = bf16_cuda(synth.normal((300, 256), 3))
-    g = f32_cuda(np.ones(256))
+    w = bf16_cuda(synth.normal((260, 64), 2))
+    r = bf16_cuda(synth.normal((300, 260), 3))
+    g = f32_cuda(np.ones(260))
     with pytest.raises(Exception):
         P().linear_residual_layernorm(a, w, r, g, g)
 
@@ -440,22 +480,57 @@ def test_layer_sequence_independence_and_permutation():
             assert rel_err(yp.float().numpy(), ref.float().numpy()) <= 1e-2
 
 
-def test_layer_virtual_ranks_equal_single_gpu():
-    # the G-shard path (each rank runs its contiguous sequence range) reproduces the 1-GPU output bitwise
-    lengths, d, H, dff = synth.config("C3")
+@pytest.mark.parametrize("cfg", ["C3", "mnli-128", "mrpc-32"])
+def test_layer_virtual_ranks_equal_single_gpu(cfg):
+    """The G-shard path (each rank runs its contiguous sequence range) reproduces the 1-GPU output BITWISE,
+    also for short-sequence batches: cora_shard_plan never splits a short-sequence window (reading s2), so
+    every rank rebuilds the 1-GPU windows of its sequences."""
+    lengths, d, H, dff = synth.config(cfg)
     w = synth.encoder_weights(d, H, dff)
     x = synth.activations(int(lengths.sum()), d)
     layer = P().EncoderLayer(P().EncoderParams.from_host(w))
-    ro = oracle.row_offsets(lengths)
     y = layer(bf16_cuda(x), _layout(lengths, H)).cpu()
     for G in (2, 4, 8):
-        plan = P().shard_plan(list(lengths), d, dff, G)
+        plan, rows = P().shard_plan(list(lengths), d, dff, G, rows=True)
+        assert plan == oracle.shard_plan(list(lengths), d, dff, G)
+        assert rows == [oracle.row_offsets(lengths)[b] for b in plan]
         parts = []
         for r in range(G):
             b0, b1 = plan[r], plan[r + 1]
             if b1 > b0:
-                parts.append(layer(bf16_cuda(x[ro[b0]:ro[b1]]), _layout(lengths[b0:b1], H)).cpu())
+                parts.append(layer(bf16_cuda(x[rows[r]:rows[r + 1]]), _layout(lengths[b0:b1], H)).cpu())
         assert torch.equal(torch.cat(parts), y)
+
+
+@pytest.mark.parametrize("cfg,n_layers,groups", [("C3", 2, 3), ("mnli-128", 3, 4), ("C1", 2, 2)])
+def test_sharded_stack_single_rank_equals_stack(cfg, n_layers, groups):
+    """cora_encoder_stack_sharded_fwd with one rank (no communicator, and a 1-rank NCCL communicator): the
+    rank's sequences in `groups` window-aligned groups, each ONE layout through every layer, equal the
+    stack on the whole batch's single layout bitwise; and the oracle stack within the stack tolerance."""
+    from paper_2110_10221_b200.dist import NcclComm, ShardedStack
+
+    lengths, d, H, dff = synth.config(cfg)
+    ws = [synth.encoder_weights(d, H, dff, seed=10 + i) for i in range(n_layers)]
+    params = [P().EncoderParams.from_host(w) for w in ws]
+    T = int(lengths.sum())
+    x = synth.activations(T, d)
+    y_ref = P().EncoderStack(params)(bf16_cuda(x), _layout(lengths, H)).cpu()
+    lt = torch.tensor(np.asarray(lengths, np.int32), device="cuda")
+    lh = torch.tensor(np.asarray(lengths, np.int32))
+    st = ShardedStack(params, n_groups=groups)
+    y = st(lt, lh, bf16_cuda(x)).cpu()
+    assert torch.equal(y, y_ref)
+    comm = NcclComm(rank=0, world=1)
+    try:
+        y2 = st(lt, lh, bf16_cuda(x), comm=comm).cpu()
+        torch.cuda.synchronize()
+        assert torch.equal(y2, y_ref)
+    finally:
+        comm.close()
+    ref = x
+    for w in ws:  # the oracle stack, chained through the bf16 storage point (reading s2 of the stack)
+        ref = synth.round_bf16(oracle.encoder_layer(ref, lengths, w))
+    assert rel_err(y.float().numpy(), ref) <= n_layers * TOL_BF16
 
 
 def test_layer_events_and_user_stream():
@@ -558,11 +633,12 @@ def test_library_nccl_allgather_single_rank():
     from paper_2110_10221_b200.dist import NcclComm, shard_rows
 
     lengths = [3, 130, 1, 64]
-    plan, tok_begin = shard_rows(lengths, 512, 2048, 1)
+    plan, row_begin = shard_rows(lengths, 512, 2048, 1)
+    assert row_begin == [0, sum(lengths)]
     comm = NcclComm(rank=0, world=1)
     out = torch.randn(sum(lengths), 512, device="cuda").to(torch.bfloat16)
     ref = out.clone()
-    comm.allgather_ragged(out, oracle.row_offsets(lengths), plan)
+    comm.allgather_ragged(out, row_begin)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)  # one rank owns every row: the in-place gather leaves them unchanged
     comm.close()
