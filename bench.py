@@ -253,6 +253,7 @@ def main():
     ap.add_argument("--groups", type=int, default=4,
                     help="N > 1 6-layer stack: groups per rank whose gather overlaps the next group's compute")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
+    ap.add_argument("--no-ex2", action="store_true", help="skip the EX2 peak microbenchmark (use under ncu)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "cora" and os.environ.get("CORA_ALLOW_FEW_WARMUP") is None:
@@ -539,7 +540,7 @@ def main():
         return
 
     peaks = load_peaks()
-    ex2 = measured_ex2_peak()
+    ex2 = None if args.no_ex2 else measured_ex2_peak()
     total_flops = useful_flops(lengths, d, dff)
     value = total_flops / (ms * 1e-3) / 1e12
     T, S2 = int(loc_len.sum()), int((loc_len ** 2).sum())

@@ -75,7 +75,7 @@ int main() {
     printf("{\"bench\": \"ex2\", \"warps_per_sm\": %d, \"gex2_per_s\": %.1f, \"ex2_per_clk_per_sm_at_max_clock\": %.2f}\n",
            wps, n / ms / 1e6, n / (ms * 1e-3) / sms / (clk * 1e3));
   }
-  for (int wps : {4, 8, 12, 16}) {
+  for (int wps : {4, 8, 12}) {
     const int iters = 512;
     k_mix<<<sms, 32 * wps>>>(out, 8, 1.f);
     cudaEventRecord(a);

@@ -64,4 +64,13 @@ for name, ev in (("no-events", None), ("events", kev)):
         b.synchronize()
         times.append(a.elapsed_time(b))
     ms = float(np.mean(times))
-    print(f"{cfg} {name}: {ms * 1e3:.1f} us/step  {flops / ms / 1e9:.1f} TFLOP/s")
+    extra = ""
+    if ev is not None:  # per-kernel means of the last replays (events recorded inside the graph)
+        per = []
+        for _ in range(20):
+            g.replay()
+            torch.cuda.synchronize()
+            per.append([kev[j].elapsed_time(kev[j + 1]) * 1e3 for j in range(7)])
+        m = np.mean(per, axis=0)
+        extra = "  [qkv %.1f attn %.1f oproj+ln1 %.1f ff1 %.1f ff2+ln2 %.1f]" % (m[0], m[1], m[2] + m[3], m[4], m[5] + m[6])
+    print(f"{cfg} {name}: {ms * 1e3:.1f} us/step  {flops / ms / 1e9:.1f} TFLOP/s{extra}", flush=True)

@@ -188,3 +188,35 @@ def test_packed_lists_cover_the_same_rows():
     assert len(pt) == len(long_items) + H * n_win
     pu = oracle.packed_unit_list(L, H)
     assert len(pu) == len([u for u in oracle.unit_list(L, H) if oracle.layout.n_q_tiles(L[u[0]]) >= 2]) + H * n_win
+
+
+# Hand-worked work lists (tile 8 for readability, 2 heads), derived on paper from reading f4-r1 (greedy
+# windows in batch order, zero-length sequences transparent, a window with >= 2 members is `packed`) and
+# the longest-first key (-q-tiles, b, h, qt) of reading c15: window order and
+# packed bits are pinned item by item.
+PACKED_CASES = [
+    (
+        [3, 4, 20, 2, 9, 1, 0, 5],  # q-tiles 1 1 3 1 2 1 0 1; windows {0,1} {3} {5,7}
+        [(0, 7, 2), (3, 2, 1), (5, 6, 2)],
+        [(2, 0, 0, 0), (2, 0, 1, 0), (2, 0, 2, 0), (2, 1, 0, 0), (2, 1, 1, 0), (2, 1, 2, 0),
+         (4, 0, 0, 0), (4, 0, 1, 0), (4, 1, 0, 0), (4, 1, 1, 0),
+         (0, 0, 0, 1), (0, 1, 0, 1), (3, 0, 0, 0), (3, 1, 0, 0), (5, 0, 0, 1), (5, 1, 0, 1)],
+        [(2, 0, 0, 0), (2, 0, 1, 0), (2, 1, 0, 0), (2, 1, 1, 0), (4, 0, 0, 0), (4, 1, 0, 0),
+         (0, 0, 0, 1), (0, 1, 0, 1), (3, 0, 0, 0), (3, 1, 0, 0), (5, 0, 0, 1), (5, 1, 0, 1)],
+    ),
+    (
+        [8, 8, 1, 7, 0, 16, 2],  # q-tiles 1 1 1 1 0 2 1; full tiles never merge; windows {0} {1} {2,3} {6}
+        [(0, 8, 1), (1, 8, 1), (2, 8, 2), (6, 2, 1)],
+        [(5, 0, 0, 0), (5, 0, 1, 0), (5, 1, 0, 0), (5, 1, 1, 0),
+         (0, 0, 0, 0), (0, 1, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (2, 0, 0, 1), (2, 1, 0, 1), (6, 0, 0, 0), (6, 1, 0, 0)],
+        [(5, 0, 0, 0), (5, 1, 0, 0),
+         (0, 0, 0, 0), (0, 1, 0, 0), (1, 0, 0, 0), (1, 1, 0, 0), (2, 0, 0, 1), (2, 1, 0, 1), (6, 0, 0, 0), (6, 1, 0, 0)],
+    ),
+]
+
+
+@pytest.mark.parametrize("L,wins,tiles,units", PACKED_CASES, ids=["mixed", "full-tiles"])
+def test_packed_lists_hand_worked(L, wins, tiles, units):
+    assert oracle.short_windows(L, tile=8) == wins
+    assert oracle.packed_tile_list(L, 2, tile=8) == tiles
+    assert oracle.packed_unit_list(L, 2, tile=8) == units
