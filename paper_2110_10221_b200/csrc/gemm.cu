@@ -380,8 +380,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 2) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
-      // shifted sums (shift K = the segment's first value): no cancellation when |mean| >> sigma
-      float s1 = 0.f, s2 = 0.f, K = 0.f;
+      // shifted sums (shift K = the segment's first value): no cancellation when |mean| >> sigma; the pair
+      // of columns of a bf16x2 word on the paired fp32 pipe (FADD2 / FFMA2)
+      float2 s1v = make_float2(0.f, 0.f), s2v = s1v, nK = s1v;
 #pragma unroll
       for (int c = 0; c < kSeg / BK; ++c) {
         uint32_t r[64];
@@ -403,15 +404,15 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
           const uint32_t rw = vv[c * 32 + p2];
           const uint32_t o = pack_bf16x2(v0 + bf16_lo(rw), v1 + bf16_hi(rw));
           vv[c * 32 + p2] = o;
-          const float y0 = bf16_lo(o), y1 = bf16_hi(o);  // statistics of the rounded values
-          if (c == 0 && p2 == 0) K = y0;
-          const float d0 = y0 - K, d1 = y1 - K;
-          s1 += d0 + d1;
-          s2 = fmaf(d0, d0, fmaf(d1, d1, s2));
+          const float2 y = make_float2(bf16_lo(o), bf16_hi(o));  // statistics of the rounded values
+          if (c == 0 && p2 == 0) nK = make_float2(-y.x, -y.x);
+          const float2 dv = __fadd2_rn(y, nK);
+          s1v = __fadd2_rn(s1v, dv);
+          s2v = __ffma2_rn(dv, dv, s2v);
         }
       }
       float2* pa = part + acc * 2 * BM;
-      pa[hf * BM + row] = seg_moments(K, s1, s2, static_cast<float>(kSeg));
+      pa[hf * BM + row] = seg_moments(-nK.x, s1v.x + s1v.y, s2v.x + s2v.y, static_cast<float>(kSeg));
       named_bar_sync(1, 32 * EW);  // both column quarters of every row are in `part`
       const float2 cm = merge_moments(pa[row], pa[BM + row], static_cast<float>(kSeg));  // this CTA's 256 columns
       if (hf == 0)
@@ -504,8 +505,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       if (u != unit0 && ew == 0 && lane == 0 && (u - unit0) / unit_step <= 2) GTRACE(10 + (u - unit0) / unit_step);
       tc_fence_after();
-      // shifted sums (shift K = the segment's first value): no cancellation when |mean| >> sigma
-      float s1 = 0.f, s2 = 0.f, K = 0.f;
+      // shifted sums (shift K = the segment's first value): no cancellation when |mean| >> sigma; the pair
+      // of columns of a bf16x2 word on the paired fp32 pipe (FADD2 / FFMA2)
+      float2 s1v = make_float2(0.f, 0.f), s2v = s1v, nK = s1v;
 #pragma unroll 1
       for (int c = 0; c < S::kBufs; ++c) {
         uint32_t r[64];
@@ -533,17 +535,17 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
             const float v0 = __uint_as_float(r[ch * 8 + 2 * i]) + bf16_lo(b2);
             const float v1 = __uint_as_float(r[ch * 8 + 2 * i + 1]) + bf16_hi(b2);
             o[i] = pack_bf16x2(v0 + bf16_lo(w[i]), v1 + bf16_hi(w[i]));
-            const float y0 = bf16_lo(o[i]), y1 = bf16_hi(o[i]);  // statistics of the rounded values
-            if (ch == 0 && i == 0 && c == 0) K = y0;
-            const float d0 = y0 - K, d1 = y1 - K;
-            s1 += d0 + d1;
-            s2 = fmaf(d0, d0, fmaf(d1, d1, s2));
+            const float2 y = make_float2(bf16_lo(o[i]), bf16_hi(o[i]));  // statistics of the rounded values
+            if (ch == 0 && i == 0 && c == 0) nK = make_float2(-y.x, -y.x);
+            const float2 dv = __fadd2_rn(y, nK);
+            s1v = __fadd2_rn(s1v, dv);
+            s2v = __ffma2_rn(dv, dv, s2v);
           }
           st_shared_v4(sbase + sw128_offset(lane, ch), o[0], o[1], o[2], o[3]);
         }
       }
       float2* pa = part + acc * (EW / 4) * BM;
-      pa[hf * BM + row] = seg_moments(K, s1, s2, static_cast<float>(S::kWarpCols));
+      pa[hf * BM + row] = seg_moments(-nK.x, s1v.x + s1v.y, s2v.x + s2v.y, static_cast<float>(S::kWarpCols));
       named_bar_sync(1, 32 * EW);  // every column group of every row is in `part`
       float2 cm = pa[row];         // this CTA's 256-column (mean, M2)
 #pragma unroll

@@ -17,6 +17,7 @@ import torch
 
 import synth
 import paper_2110_10221_b200 as P
+from bench import tile_waste
 
 
 def main():
@@ -62,15 +63,15 @@ def main():
         useful = 2 * T * (4 * d * d + 2 * d * dff) + 4 * d * S2
         Lp = int(lengths.max())
         padded = 2 * len(lengths) * Lp * (4 * d * d + 2 * d * dff) + 4 * d * len(lengths) * Lp * Lp
-        nq = (lengths + 127) // 128
-        tile_work = int((nq * nq).sum()) * 128 * 128
+        # masked share of the attention work actually run, from the device work list (packed windows included)
+        waste = tile_waste(P.layout_build(Lt, T, H, 512), H)
         print(json.dumps({
             "config": cfg, "batch": int(len(lengths)), "total_tokens": T, "sum_L2": S2, "max_len": Lp,
             "ms_per_step_p50": ms, "ms_p10": float(np.percentile(times, 10)), "ms_p90": float(np.percentile(times, 90)),
             "useful_tflops": useful / (ms * 1e-3) / 1e12,
             "frac_of_burst_peak": useful / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
             "padded_over_useful_flops": padded / useful,
-            "attention_tile_waste": 1.0 - S2 / tile_work if tile_work else 0.0,
+            "attention_tile_waste": waste["waste"], "attention_work_items": waste["work_items"],
         }), flush=True)
 
 
