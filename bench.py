@@ -254,6 +254,10 @@ def main():
                     help="N > 1 6-layer stack: groups per rank whose gather overlaps the next group's compute")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
     ap.add_argument("--no-ex2", action="store_true", help="skip the EX2 peak microbenchmark (use under ncu)")
+    ap.add_argument("--debug-gloo", action="store_true",
+                    help="N > 1 control-flow check on ONE GPU: ranks share the device, gloo process group, the "
+                         "gather through torch.distributed (the library's NCCL path needs one GPU per rank); "
+                         "not a measurement")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "cora" and os.environ.get("CORA_ALLOW_FEW_WARMUP") is None:
@@ -273,10 +277,15 @@ def main():
     import paper_2110_10221_b200 as P
     from paper_2110_10221_b200.dist import NcclComm, ShardedStack, shard_rows
 
+    if args.debug_gloo:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.debug_gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     # ---------------------------------------------------------------- workload (synthetic, seeded)
     w = synth.encoder_weights(d, H, dff)
@@ -324,10 +333,15 @@ def main():
         return lay
 
     # N > 1: the library's own NCCL communicator and in-place ragged all-gather (cora_allgather_ragged)
-    lib_comm = NcclComm(rank, world) if world > 1 else None
+    lib_comm = NcclComm(rank, world) if world > 1 and not args.debug_gloo else None
 
     def gather():
-        lib_comm.allgather_ragged(y_full, row_begin)
+        if lib_comm is not None:
+            lib_comm.allgather_ragged(y_full, row_begin)
+        else:  # --debug-gloo: the same in-place schedule through torch.distributed
+            for r in range(world):
+                if row_begin[r + 1] > row_begin[r]:
+                    dist.broadcast(y_full[row_begin[r]:row_begin[r + 1]], src=r)
 
     # correctness gate on the benchmarked configuration (status word)
     lay = step()
@@ -444,7 +458,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         g_ms, sg_ms = (float(v) for v in t.tolist())
         gather_info = {"allgather_ms": g_ms, "bytes_received_per_rank": int((T_all - T_loc) * d * 2),
-                       "path": "cora_allgather_ragged (the library's NCCL communicator, grouped in-place broadcasts)",
+                       "path": ("torch.distributed gloo broadcasts (--debug-gloo control-flow check, ranks share one GPU)"
+                                if args.debug_gloo else
+                                "cora_allgather_ragged (the library's NCCL communicator, grouped in-place broadcasts)"),
                        "with_gather": {"ms_per_step": sg_ms,
                                        "value": useful_flops(lengths, d, dff) / (sg_ms * 1e-3) / 1e12,
                                        "unit": "TFLOP/s"},
@@ -456,7 +472,7 @@ def main():
     # one layout (prelude) per batch shared by 6 layers, one CUDA graph per
     # step, L2 flushed between steps like the headline number; reported beside it, not instead of it
     stack = None
-    if not args.no_stack:
+    if not args.no_stack and not (world > 1 and args.debug_gloo):
         stack_params = [P.EncoderParams.from_host(synth.encoder_weights(d, H, dff, seed=200 + i), device=dev)
                         for i in range(6)]
         n_stack = max(3, min(args.steps, 50))
