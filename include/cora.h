@@ -274,21 +274,28 @@ cora_status_t cora_layernorm_fwd(const void* x, const void* residual, const floa
  * The paper's matrix-multiplication workloads (Sec. "Matrix Multiplication"), bf16
  * inputs, fp32 accumulation in TMEM, bf16 outputs, one persistent tcgen05 kernel (128 x 256 tiles). */
 
-/* Workspace for cora_vgemm_fwd: the device work list (16 B per 128 x 256 output tile) and the problem
- * dims; 0 on invalid arguments.  dims_host: [batch][3] = (M_i, N_i, K_i). */
+/* Bytes of the serialised vgemm work list ("plan") of these problems (0 on invalid arguments); also the
+ * device workspace cora_vgemm_fwd needs.  dims_host: [batch][3] = (M_i, N_i, K_i). */
+size_t cora_vgemm_plan_bytes(int32_t batch, const int32_t* dims_host);
 size_t cora_vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host);
 
-/* Variable-sized batched GEMM: C_i = A_i B_i for i < batch, each problem with its own
- * (M_i, N_i, K_i).  Fully padded storage as in the paper's evaluation: a = A
+/* Build the work list of cora_vgemm_fwd on the host into caller memory plan_host (>= cora_vgemm_plan_bytes):
+ * every 128 x 256 output tile of every problem, scheduled longest reduction first (stable).  Validation:
+ * M_i <= m_max, N_i <= n_max, K_i <= k_max, n_max % 8 == 0, k_max % 8 == 0 (CORA_ERR_INVALID); K_i % 64 == 0
+ * unless K_i == k_max (a partial last k-block would read A/B padding: CORA_ERR_UNSUPPORTED). */
+cora_status_t cora_vgemm_plan(int32_t batch, const int32_t* dims_host, int32_t m_max, int32_t n_max, int32_t k_max,
+                              void* plan_host, size_t plan_bytes);
+
+/* Variable-sized batched GEMM: C_i = A_i B_i for every problem of the plan, each with its
+ * own (M_i, N_i, K_i).  Fully padded storage as in the paper's evaluation: a = A
  * [batch, m_max, k_max], b = B [batch, k_max, n_max], c = C [batch, m_max, n_max], row-major bf16 device
- * buffers (caller-owned).  Only C_i[:M_i, :N_i] is written (the padding of c is left untouched) and only
- * K_i of each reduction is visited.  Tiles are scheduled longest reduction first.  The work list is built
- * on the host from dims_host and copied into ws on `stream` (a pageable host-to-device copy).
- * Requires n_max % 8 == 0, k_max % 8 == 0, 16-B aligned pointers, M_i <= m_max, N_i <= n_max, K_i <= k_max;
- * K_i % 64 == 0 unless K_i == k_max (a partial last k-block would read A/B padding:
- * CORA_ERR_UNSUPPORTED).  batch == 0 is a no-op.  CORA_ERR_INVALID on bad arguments / small ws. */
-cora_status_t cora_vgemm_fwd(int32_t batch, const int32_t* dims_host, const void* a, const void* b, void* c,
-                             int32_t m_max, int32_t n_max, int32_t k_max, void* ws, size_t ws_bytes, void* stream);
+ * buffers (caller-owned).  Only C_i[:M_i, :N_i] is written (the padding of c is left untouched; K_i == 0
+ * gives C_i = 0) and only K_i of each reduction is visited.  The plan (cora_vgemm_plan) is copied into ws
+ * (>= cora_vgemm_workspace_bytes) with one cudaMemcpyAsync on `stream`: from PINNED host memory the call is
+ * stream-capturable (a memcpy node that re-reads plan_host at every replay; keep it alive and unchanged).
+ * 16-B aligned pointers.  An empty plan is a no-op.  CORA_ERR_INVALID on bad arguments / small ws. */
+cora_status_t cora_vgemm_fwd(const void* plan_host, const void* a, const void* b, void* c, int32_t m_max, int32_t n_max,
+                             int32_t k_max, void* ws, size_t ws_bytes, void* stream);
 
 /* Triangular matrix multiplication: c[n, n_cols] = tril(l) b, l [n, n] and
  * b [n, n_cols] row-major bf16.  Only the lower triangle of l (diagonal included) is read (BLAS trmm

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     EncoderStack,
     HostForward,
     RaggedLayout,
+    VgemmPlan,
     build_info,
     encoder_layer,
     layernorm,

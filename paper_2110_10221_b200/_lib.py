@@ -23,7 +23,7 @@ LAYER_EVENTS = 8
 EXPORTS = (
     "cora_layout_workspace_bytes", "cora_layout_build", "cora_layout_status", "cora_encoder_workspace_bytes",
     "cora_encoder_layer_fwd", "cora_encoder_layer_fwd_ex", "cora_encoder_layer_launches", "cora_encoder_stack_workspace_bytes", "cora_encoder_stack_fwd", "cora_encoder_forward_workspace_bytes", "cora_encoder_forward", "cora_forward_host_workspace_bytes",
-    "cora_encoder_forward_host", "cora_linear_fwd", "cora_linear_residual_layernorm_fwd", "cora_vgemm_workspace_bytes", "cora_vgemm_fwd", "cora_trmm_fwd", "cora_ragged_attention_fwd", "cora_ragged_masked_attention_fwd", "cora_ragged_softmax_fwd",
+    "cora_encoder_forward_host", "cora_linear_fwd", "cora_linear_residual_layernorm_fwd", "cora_vgemm_plan_bytes", "cora_vgemm_workspace_bytes", "cora_vgemm_plan", "cora_vgemm_fwd", "cora_trmm_fwd", "cora_ragged_attention_fwd", "cora_ragged_masked_attention_fwd", "cora_ragged_softmax_fwd",
     "cora_layernorm_fwd", "cora_shard_plan", "cora_shard_groups", "cora_encoder_stack_sharded_workspace_bytes",
     "cora_encoder_stack_sharded_fwd", "cora_comm_unique_id_bytes", "cora_comm_get_unique_id", "cora_comm_init", "cora_comm_destroy", "cora_allgather_ragged", "cora_status_string", "cora_device_sm_count", "cora_build_info",
 )
@@ -97,8 +97,10 @@ def lib() -> ctypes.CDLL:
                                                 ctypes.POINTER(Layout), vp]),
             "cora_linear_fwd": (i32, [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]),
             "cora_linear_residual_layernorm_fwd": (i32, [vp, vp, vp, vp, vp, vp, f32, vp, i32, i32, i32, i32, vp]),
+            "cora_vgemm_plan_bytes": (sz, [i32, vp]),
             "cora_vgemm_workspace_bytes": (sz, [i32, vp]),
-            "cora_vgemm_fwd": (i32, [i32, vp, vp, vp, vp, i32, i32, i32, vp, sz, vp]),
+            "cora_vgemm_plan": (i32, [i32, vp, i32, i32, i32, vp, sz]),
+            "cora_vgemm_fwd": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, sz, vp]),
             "cora_trmm_fwd": (i32, [vp, vp, vp, i32, i32, vp]),
             "cora_ragged_attention_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, f32, vp]),
             "cora_ragged_masked_attention_fwd": (i32, [ctypes.POINTER(Layout), vp, vp, i32, f32, vp]),

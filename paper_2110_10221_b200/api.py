@@ -317,25 +317,46 @@ def linear_residual_layernorm(a: torch.Tensor, w: torch.Tensor, residual: torch.
     return c
 
 
-def vgemm(a: torch.Tensor, b: torch.Tensor, dims, out: Optional[torch.Tensor] = None,
-          stream=None) -> torch.Tensor:
+class VgemmPlan:
+    """The serialised vgemm work list (cora_vgemm_plan) in PINNED host memory, and its device workspace:
+    reusable, and capturable in a CUDA graph (the plan copy is a memcpy node from pinned memory)."""
+
+    def __init__(self, dims, m_max: int, n_max: int, k_max: int, device="cuda"):
+        batch = len(dims)
+        if any(len(row) != 3 for row in dims):
+            raise ValueError("dims: [batch][3] (M_i, N_i, K_i)")
+        self.dims = [tuple(int(v) for v in row) for row in dims]
+        self.shape = (batch, int(m_max), int(n_max), int(k_max))
+        dh = (ctypes.c_int32 * max(3 * batch, 1))(*[v for row in self.dims for v in row])
+        n = int(C.lib().cora_vgemm_plan_bytes(batch, dh))
+        if n == 0:
+            raise C.CoraError(C.CORA_ERR_INVALID, "cora_vgemm_plan_bytes")
+        self.host = torch.empty(n, dtype=torch.uint8).pin_memory()
+        C.check(C.lib().cora_vgemm_plan(batch, dh, int(m_max), int(n_max), int(k_max), ctypes.c_void_p(self.host.data_ptr()),
+                                        n), "cora_vgemm_plan")
+        self.ws = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
+
+def vgemm(a: torch.Tensor, b: torch.Tensor, dims, out: Optional[torch.Tensor] = None, stream=None,
+          plan: Optional[VgemmPlan] = None) -> torch.Tensor:
     """C_i = A_i B_i over padded buffers a [batch, M_max, K_max], b [batch, K_max, N_max] (bf16); dims:
-    [batch][3] host ints (M_i, N_i, K_i).  Returns c [batch, M_max, N_max]; only C_i[:M_i, :N_i] is
-    written (the rest of `out` is left as it was; a fresh `out` is zero-filled)."""
+    [batch][3] host ints (M_i, N_i, K_i) (or a prebuilt `plan`).  Returns c [batch, M_max, N_max]; only
+    C_i[:M_i, :N_i] is written (the rest of `out` is left as it was; a fresh `out` is zero-filled)."""
     _need_cuda(a, b, out)
     batch, m_max, k_max = a.shape
     n_max = b.shape[2]
     if b.shape[:2] != (batch, k_max) or a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise ValueError("a [batch, M_max, K_max], b [batch, K_max, N_max], bf16")
-    if len(dims) != batch or any(len(row) != 3 for row in dims):
-        raise ValueError("dims: [batch][3] (M_i, N_i, K_i)")
+    if plan is None:
+        if len(dims) != batch:
+            raise ValueError("dims: [batch][3] (M_i, N_i, K_i)")
+        plan = VgemmPlan(dims, m_max, n_max, k_max, device=a.device)
+    elif plan.shape != (batch, m_max, n_max, k_max):
+        raise ValueError("plan built for other buffer shapes")
     _expect(out, (batch, m_max, n_max), torch.bfloat16, "out", a.device)
-    dh = (ctypes.c_int32 * (3 * batch))(*[int(v) for row in dims for v in row])
     c = torch.zeros(batch, m_max, n_max, dtype=torch.bfloat16, device=a.device) if out is None else out
-    nbytes = int(C.lib().cora_vgemm_workspace_bytes(batch, dh))
-    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=a.device)
-    C.check(C.lib().cora_vgemm_fwd(batch, dh, _ptr(a), _ptr(b), _ptr(c), m_max, n_max, k_max, _ptr(ws), nbytes,
-                                   _stream(stream)), "cora_vgemm_fwd")
+    C.check(C.lib().cora_vgemm_fwd(ctypes.c_void_p(plan.host.data_ptr()), _ptr(a), _ptr(b), _ptr(c), m_max, n_max, k_max,
+                                   _ptr(plan.ws), plan.ws.numel(), _stream(stream)), "cora_vgemm_fwd")
     return c
 
 

@@ -250,29 +250,44 @@ cora_status_t cora_linear_residual_layernorm_fwd(const void* a, const void* w, c
   return cuda_status(e);
 }
 
-size_t cora_vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host) {
+size_t cora_vgemm_plan_bytes(int32_t batch, const int32_t* dims_host) {
   if (batch < 0 || (batch > 0 && dims_host == nullptr)) return 0;
   for (int i = 0; i < batch; ++i)
     if (dims_host[3 * i] < 0 || dims_host[3 * i + 1] < 0 || dims_host[3 * i + 2] < 0) return 0;
-  return vgemm_workspace_bytes(batch, dims_host);
+  return vgemm_plan_bytes(batch, dims_host);
 }
 
-cora_status_t cora_vgemm_fwd(int32_t batch, const int32_t* dims_host, const void* a, const void* b, void* c,
-                             int32_t m_max, int32_t n_max, int32_t k_max, void* ws, size_t ws_bytes, void* stream) {
-  if (batch < 0 || m_max < 0 || n_max < 0 || k_max < 0) return CORA_ERR_INVALID;
-  if (batch == 0 || m_max == 0 || n_max == 0) return CORA_OK;
-  if (dims_host == nullptr || a == nullptr || b == nullptr || c == nullptr || ws == nullptr) return CORA_ERR_INVALID;
-  if (!aligned16(a) || !aligned16(b) || !aligned16(c) || !aligned16(ws) || (n_max % 8) != 0 || (k_max % 8) != 0 ||
-      k_max == 0)
-    return CORA_ERR_INVALID;
+size_t cora_vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host) {
+  return cora_vgemm_plan_bytes(batch, dims_host);
+}
+
+cora_status_t cora_vgemm_plan(int32_t batch, const int32_t* dims_host, int32_t m_max, int32_t n_max, int32_t k_max,
+                              void* plan_host, size_t plan_bytes) {
+  if (batch < 0 || m_max < 0 || n_max < 0 || k_max < 0 || plan_host == nullptr) return CORA_ERR_INVALID;
+  if (batch > 0 && dims_host == nullptr) return CORA_ERR_INVALID;
+  if ((n_max % 8) != 0 || (k_max % 8) != 0) return CORA_ERR_INVALID;
   for (int i = 0; i < batch; ++i) {
     const int32_t m = dims_host[3 * i], n = dims_host[3 * i + 1], k = dims_host[3 * i + 2];
     if (m < 0 || n < 0 || k < 0 || m > m_max || n > n_max || k > k_max) return CORA_ERR_INVALID;
     // a partial last k-block would read the padding of A and B unless it is the tensor's own tail
     if ((k % 64) != 0 && k != k_max) return CORA_ERR_UNSUPPORTED;
   }
-  if (ws_bytes < vgemm_workspace_bytes(batch, dims_host)) return CORA_ERR_INVALID;
-  return cuda_status(launch_vgemm(batch, dims_host, a, b, c, m_max, n_max, k_max, ws, as_stream(stream)));
+  if (plan_bytes < vgemm_plan_bytes(batch, dims_host)) return CORA_ERR_INVALID;
+  vgemm_plan(batch, dims_host, plan_host);
+  return CORA_OK;
+}
+
+cora_status_t cora_vgemm_fwd(const void* plan_host, const void* a, const void* b, void* c, int32_t m_max, int32_t n_max,
+                             int32_t k_max, void* ws, size_t ws_bytes, void* stream) {
+  if (plan_host == nullptr || m_max < 0 || n_max < 0 || k_max < 0) return CORA_ERR_INVALID;
+  const int32_t* h = static_cast<const int32_t*>(plan_host);
+  if (h[1] == 0 || h[2] == 0 || m_max == 0 || n_max == 0) return CORA_OK;  // nothing to compute
+  if (a == nullptr || b == nullptr || c == nullptr || ws == nullptr) return CORA_ERR_INVALID;
+  if (!aligned16(a) || !aligned16(b) || !aligned16(c) || !aligned16(ws) || (n_max % 8) != 0 || (k_max % 8) != 0 ||
+      k_max == 0)
+    return CORA_ERR_INVALID;
+  if (!vgemm_plan_valid(plan_host, ws_bytes)) return CORA_ERR_INVALID;
+  return cuda_status(launch_vgemm(plan_host, a, b, c, m_max, n_max, k_max, ws, as_stream(stream)));
 }
 
 cora_status_t cora_trmm_fwd(const void* l, const void* b, void* c, int32_t n, int32_t n_cols, void* stream) {

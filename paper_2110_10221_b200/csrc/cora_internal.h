@@ -39,9 +39,11 @@ bool gemm_ln_supported(const GemmArgs& g);
 cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream);
 
 // vgemm / trmm (vgemm.cu, SURVEY f-3)
-size_t vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host);
-cudaError_t launch_vgemm(int32_t batch, const int32_t* dims_host, const void* a, const void* b, void* c,
-                         int32_t m_max, int32_t n_max, int32_t k_max, void* ws, cudaStream_t stream);
+size_t vgemm_plan_bytes(int32_t batch, const int32_t* dims_host);
+void vgemm_plan(int32_t batch, const int32_t* dims_host, void* plan_host);
+bool vgemm_plan_valid(const void* plan_host, size_t ws_bytes);
+cudaError_t launch_vgemm(const void* plan_host, const void* a, const void* b, void* c, int32_t m_max, int32_t n_max,
+                         int32_t k_max, void* ws, cudaStream_t stream);
 cudaError_t launch_trmm(const void* l, const void* b, void* c, int32_t n, int32_t n_cols, cudaStream_t stream);
 
 cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,

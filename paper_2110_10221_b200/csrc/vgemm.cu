@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "cora_internal.h"
@@ -261,34 +262,55 @@ cudaError_t set_smem_attr() {
 
 }  // namespace
 
-size_t vgemm_workspace_bytes(int32_t batch, const int32_t* dims_host) {
+// Serialised work list ("plan"): a 16-byte header {magic, batch, n_units, 0}, the units (16 B each: every
+// 128 x 256 tile of every problem, longest reduction first, stable) and the problems' (M_i, N_i).  Built on
+// the host into caller memory, copied verbatim into the device workspace by launch_vgemm.
+constexpr int32_t kPlanMagic = 0x56474D31;  // "VGM1"
+size_t vgemm_plan_bytes(int32_t batch, const int32_t* dims_host) {
   size_t units = 0;
   for (int i = 0; i < batch; ++i)
     units += static_cast<size_t>((dims_host[3 * i] + VM - 1) / VM) * ((dims_host[3 * i + 1] + VN - 1) / VN);
-  return 256 + units * sizeof(VUnit) + static_cast<size_t>(batch) * sizeof(ProblemDims);
+  return 16 + units * sizeof(VUnit) + static_cast<size_t>(batch) * sizeof(ProblemDims);
 }
 
-cudaError_t launch_vgemm(int32_t batch, const int32_t* dims_host, const void* a, const void* b, void* c,
-                         int32_t m_max, int32_t n_max, int32_t k_max, void* ws, cudaStream_t stream) {
-  // host-side work list: every 128 x 256 tile of every problem, longest reduction first (stable)
+void vgemm_plan(int32_t batch, const int32_t* dims_host, void* plan_host) {
   std::vector<VUnit> units;
-  std::vector<ProblemDims> pd(batch);
   for (int i = 0; i < batch; ++i) {
     const int m = dims_host[3 * i], n = dims_host[3 * i + 1], k = dims_host[3 * i + 2];
-    pd[i] = ProblemDims{m, n};
     const int kb = (k + VK - 1) / VK;
     for (int m0 = 0; m0 < m; m0 += VM)
       for (int n0 = 0; n0 < n; n0 += VN) units.push_back(VUnit{i, m0, n0, kb});
   }
   std::stable_sort(units.begin(), units.end(), [](const VUnit& x, const VUnit& y) { return x.kb > y.kb; });
-  if (units.empty()) return cudaSuccess;
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  VUnit* d_units = reinterpret_cast<VUnit*>(w + 256);
-  ProblemDims* d_dims = reinterpret_cast<ProblemDims*>(w + 256 + units.size() * sizeof(VUnit));
-  cudaError_t e = cudaMemcpyAsync(d_units, units.data(), units.size() * sizeof(VUnit), cudaMemcpyHostToDevice, stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d_dims, pd.data(), pd.size() * sizeof(ProblemDims), cudaMemcpyHostToDevice, stream);
+  int32_t* h = static_cast<int32_t*>(plan_host);
+  h[0] = kPlanMagic;
+  h[1] = batch;
+  h[2] = static_cast<int32_t>(units.size());
+  h[3] = 0;
+  uint8_t* p = static_cast<uint8_t*>(plan_host) + 16;
+  if (!units.empty()) std::memcpy(p, units.data(), units.size() * sizeof(VUnit));
+  ProblemDims* pd = reinterpret_cast<ProblemDims*>(p + units.size() * sizeof(VUnit));
+  for (int i = 0; i < batch; ++i) pd[i] = ProblemDims{dims_host[3 * i], dims_host[3 * i + 1]};
+}
+
+bool vgemm_plan_valid(const void* plan_host, size_t ws_bytes) {
+  const int32_t* h = static_cast<const int32_t*>(plan_host);
+  if (h[0] != kPlanMagic || h[1] < 0 || h[2] < 0) return false;
+  return 16 + static_cast<size_t>(h[2]) * sizeof(VUnit) + static_cast<size_t>(h[1]) * sizeof(ProblemDims) <= ws_bytes;
+}
+
+cudaError_t launch_vgemm(const void* plan_host, const void* a, const void* b, void* c, int32_t m_max, int32_t n_max,
+                         int32_t k_max, void* ws, cudaStream_t stream) {
+  const int32_t* h = static_cast<const int32_t*>(plan_host);
+  const int32_t batch = h[1], n_units = h[2];
+  if (n_units == 0) return cudaSuccess;
+  // one asynchronous copy of the plan: from pinned caller memory it is a graph-capturable memcpy node
+  const size_t bytes = 16 + static_cast<size_t>(n_units) * sizeof(VUnit) + static_cast<size_t>(batch) * sizeof(ProblemDims);
+  cudaError_t e = cudaMemcpyAsync(ws, plan_host, bytes, cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return e;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const VUnit* d_units = reinterpret_cast<const VUnit*>(w + 16);
+  const ProblemDims* d_dims = reinterpret_cast<const ProblemDims*>(w + 16 + static_cast<size_t>(n_units) * sizeof(VUnit));
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, a, k_max, static_cast<uint64_t>(batch) * m_max, static_cast<uint64_t>(k_max) * 2, VK,
                          VM, true) ||
@@ -296,10 +318,10 @@ cudaError_t launch_vgemm(int32_t batch, const int32_t* dims_host, const void* a,
                          VK, true))
     return cudaErrorInvalidValue;
   if ((e = set_smem_attr<false>()) != cudaSuccess) return e;
-  const int n_units = static_cast<int>(units.size());
-  const int grid = std::min(n_units, device_sm_count());
+  const int grid = std::min(static_cast<int>(n_units), device_sm_count());
   return launch_pdl(vgemm_kernel<false>, dim3(grid), dim3(kVThreads), kSmemBytes, stream, 1, ta, tb, d_units, d_dims,
-                    n_units, m_max, k_max, static_cast<__nv_bfloat16*>(c), static_cast<int64_t>(n_max), 0, 0, 0, 0);
+                    static_cast<int>(n_units), m_max, k_max, static_cast<__nv_bfloat16*>(c), static_cast<int64_t>(n_max),
+                    0, 0, 0, 0);
 }
 
 cudaError_t launch_trmm(const void* l, const void* b, void* c, int32_t n, int32_t n_cols, cudaStream_t stream) {

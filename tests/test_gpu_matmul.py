@@ -54,6 +54,33 @@ def test_vgemm_paper_workload_sample():
         assert rel_err(c[i, :m, :n], ref[i]) <= TOL_BF16
 
 
+def test_vgemm_in_a_cuda_graph():
+    """The plan lives in pinned host memory, so the call (plan copy + kernel) is stream-capturable; a replay
+    recomputes C after the inputs change."""
+    dims = [(300, 200, 256), (128, 264, 64), (0, 8, 64), (257, 64, 128)]
+    mm, nn, kk = 300, 264, 256
+    a = synth.round_bf16(synth.normal((4, mm, kk), 31))
+    b = synth.round_bf16(synth.normal((4, kk, nn), 32) / np.sqrt(kk))
+    ta, tb = bf16_cuda(a), bf16_cuda(b)
+    c = torch.zeros(4, mm, nn, dtype=torch.bfloat16, device="cuda")
+    plan = P().VgemmPlan(dims, mm, nn, kk)
+    P().vgemm(ta, tb, dims, out=c, plan=plan)  # warm-up (function attributes, tensor-map encoder)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        P().vgemm(ta, tb, dims, out=c, plan=plan)
+    a2 = synth.round_bf16(synth.normal((4, mm, kk), 33))
+    ta.copy_(bf16_cuda(a2))
+    c.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ref = oracle.vgemm(a2, b, dims)
+    got = to_np(c)
+    for i, (m, n, k) in enumerate(dims):
+        if m and n:
+            assert rel_err(got[i, :m, :n], ref[i]) <= TOL_BF16
+
+
 def test_vgemm_rejects_partial_k_block_inside_padding():
     a = bf16_cuda(np.zeros((2, 64, 128)))
     b = bf16_cuda(np.zeros((2, 128, 64)))
