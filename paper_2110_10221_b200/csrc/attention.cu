@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "cora_internal.h"
 #include "ptx.cuh"
@@ -46,7 +47,17 @@ constexpr int TK = 128;       // keys per KV tile
 constexpr int QSTAGES = 2;    // Q double buffer: the next tile's Q streams in under the current tile
 constexpr int KSTAGES = 3;    // K ring depth
 constexpr int VSTAGES = 2;    // V ring depth
-constexpr int kThreads = 192;
+// Warp roles.  Bidirectional kernel (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
+// warps 2-5 softmax.  Causal kernel (256 threads): warps 0 / 1 the same, warps 2-3 idle (they complete
+// warpgroup 0, whose registers go to the softmax warpgroup), warps 4-7 softmax.  Warp w of the softmax
+// reads TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31.
+template <bool CAUSAL>
+constexpr int kThreadsOf = CAUSAL ? 256 : 192;
+template <bool CAUSAL>
+constexpr uint32_t kSoftmaxWarp0 = CAUSAL ? 4 : 2;
+// causal: 2 CTAs x 256 threads x 128 registers at launch; setmaxnreg: 128 x 56 + 128 x 200 = 256 x 128 (the
+// per-chunk liveness of the diagonal / tail tiles needs more than the 168 registers of 192 threads)
+constexpr uint32_t kRegsSoftmax = 200, kRegsOther = 56;
 constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
 // Lazy rescaling (reading a3-r1): the running reference max m_ref of a row is only
 // moved when a new score exceeds it by more than kRescaleLog2 (in log2 units), so P <= 2^8 and the
@@ -124,7 +135,7 @@ __device__ __forceinline__ WorkUnit load_work(const int32_t* list, const int2* l
 // q-tile qt needs only KV tiles j <= qt (the "lower triangular" ragged loop -- tiles above the diagonal
 // are never loaded or computed) and the diagonal tile is masked per element.
 template <bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
                          const int2* __restrict__ tile_seq, const int32_t* __restrict__ n_tiles_ptr,
                          const int32_t* __restrict__ seq_of_tok, const int32_t* __restrict__ pos_in_seq,
@@ -175,14 +186,28 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_ptr;
+  // tmem_base / n_tiles / the first work unit: read before the role split (bidirectional), or by each role
+  // after its register reallocation (causal: values live across setmaxnreg are spilled)
+  uint32_t tmem_base = 0;
+  int n_tiles = 0;
+  WorkUnit wu_next{};
+  if constexpr (!CAUSAL) tmem_base = *tmem_ptr;
   pdl_wait();  // QKV (previous kernel) complete and visible
   pdl_trigger();
-  const int n_tiles = *n_tiles_ptr;
-  // every role walks the same tiles; the next tile's metadata load is issued one tile ahead
-  WorkUnit wu_next{};
-  if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
+  if constexpr (!CAUSAL) {
+    n_tiles = *n_tiles_ptr;
+    // every role walks the same tiles; the next tile's metadata load is issued one tile ahead
+    if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
+  }
 
+  if (warp < kSoftmaxWarp0<CAUSAL>) {
+    // causal: warpgroup 0 (producer, MMA issuer, two idle warps) hands its registers to the softmax warpgroup
+    if constexpr (CAUSAL) {
+      setmaxnreg_dec<kRegsOther>();
+      tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
+      n_tiles = *n_tiles_ptr;
+      if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
+    }
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producers
     // lane 0 streams Q and K, lane 1 streams V: the two rings are refilled independently, so a V slot
@@ -284,8 +309,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
+  }
   } else {
     // ------------------------------------------------------------ softmax / correction / epilogue
+    if constexpr (CAUSAL) {
+      setmaxnreg_inc<kRegsSoftmax>();
+      tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
+      n_tiles = *n_tiles_ptr;
+    }
     const uint32_t qd = warp & 3;  // TMEM lane quadrant
     const bool out_v8 = (reinterpret_cast<uintptr_t>(out) & 31u) == 0 && (d_model % 16) == 0 && (HD % 16) == 0;
     const int i = qd * 32 + lane;  // query row within the tile
@@ -293,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t s_ph = 0, pv_ph = 0;
     // the next tile's metadata is prefetched one tile ahead into shared memory with cp.async (no
     // registers held while in flight; prefetching into registers spilled)
-    int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + (warp - 2) * 2;  // [2 slots] per warp
+    int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + qd * 2;  // [2 slots] per warp
     auto prefetch_meta = [&](int idx, int slot) {
       if (lane == 0 && idx < n_tiles) {
         cp_async_4(&meta[slot].x, tiles + idx);
@@ -351,6 +382,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         float m_ref = -INFINITY, l = 0.f;
         for (int j = 0; j < nkv; ++j) {
           const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
+          const bool diag = CAUSAL && j == cur.qt;
+          // leading 32-key chunks holding a key visible to some row of this warp (warp-uniform): a tail tile
+          // stops at the last valid key, a causal diagonal tile at this warp's last row; the chunks after
+          // them are not exponentiated -- their P is 0
+          // (causal kernel only: the bidirectional one keeps every chunk live -- within its 168 registers
+          // per-chunk liveness spills -- and masks the tail tile element by element)
+          int live = TK / 32;
+          if constexpr (CAUSAL) {
+            if (valid < TK) live = (valid + 31) >> 5;
+            if (diag && live > static_cast<int>(qd) + 1) live = static_cast<int>(qd) + 1;
+            if (cur.packed) live = TK / 32;
+          }
           mbar_wait<false>(s_full, s_ph);
           s_ph ^= 1;
           tc_fence_after();
@@ -363,9 +406,9 @@ __global__ void __launch_bounds__(kThreads, 2)
           __syncwarp();
           if (lane == 0) mbar_arrive(s_empty);
           float* sv = reinterpret_cast<float*>(sr);
-          // row max over the valid keys (keys >= L_b masked to -inf in the tail tile; with CAUSAL also the
-          // keys after the query in the diagonal tile)
-          const bool masked = (CAUSAL && j == cur.qt) || valid < TK || cur.packed;
+          // keys >= L_b (tail tile) and, with CAUSAL, keys after the query (diagonal tile) get -inf before the
+          // row max (reading c18); only the last live chunk can hold such keys
+          const bool masked = diag || valid < TK || cur.packed;
           if (cur.packed) {  // block-diagonal (one KV tile: j == 0 == qt)
             // keys [lo, hi) of the window belong to this row's sequence (f_fo / f_fi maps of the prelude)
             int lo = 0, hi = 0;
@@ -377,20 +420,44 @@ __global__ void __launch_bounds__(kThreads, 2)
   #pragma unroll
             for (int c = 0; c < TK; ++c)
               if (c < lo || c >= hi || (CAUSAL && c > i)) sv[c] = -INFINITY;
-          } else if (CAUSAL && j == cur.qt) {
-  #pragma unroll
-            for (int c = 0; c < TK; ++c)
-              if (c > i || c >= valid) sv[c] = -INFINITY;
-          } else if (valid < TK) {
+          } else if (!CAUSAL && valid < TK) {
   #pragma unroll
             for (int c = 0; c < TK; ++c)
               if (c >= valid) sv[c] = -INFINITY;
+          } else if (masked) {
+            const int hi = diag ? min(valid, i + 1) : valid;
+            auto mask_chunk = [&](auto cb_tag) {
+              constexpr int cb = decltype(cb_tag)::value;
+              if (cb == live - 1) {
+  #pragma unroll
+                for (int c = cb * 32; c < cb * 32 + 32; ++c)
+                  if (c >= hi) sv[c] = -INFINITY;
+              }
+            };
+            mask_chunk(std::integral_constant<int, 0>{});
+            mask_chunk(std::integral_constant<int, 1>{});
+            mask_chunk(std::integral_constant<int, 2>{});
+            mask_chunk(std::integral_constant<int, 3>{});
           }
           float m8[8];
   #pragma unroll
           for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+          auto max_chunk = [&](auto cb_tag) {
+            constexpr int cb = decltype(cb_tag)::value;
+            if (cb < live) {
   #pragma unroll
-          for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+              for (int c = cb * 32; c < cb * 32 + 32; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+            }
+          };
+          if constexpr (CAUSAL) {
+            max_chunk(std::integral_constant<int, 0>{});
+            max_chunk(std::integral_constant<int, 1>{});
+            max_chunk(std::integral_constant<int, 2>{});
+            max_chunk(std::integral_constant<int, 3>{});
+          } else {
+  #pragma unroll
+            for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
+          }
           const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                  fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
           // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
@@ -404,20 +471,50 @@ __global__ void __launch_bounds__(kThreads, 2)
   #pragma unroll
           for (int k = 0; k < 8; ++k) r8[k] = 0.f;
           uint32_t pk[TK / 2];
+          auto exp_chunk = [&](auto cb_tag) {
+            constexpr int cb = decltype(cb_tag)::value;
+            if (cb < live) {
   #pragma unroll
-          for (int c = 0; c < TK; c += 2) {
-            const float x0 = fmaf(sv[c], scale_log2, -m_ref), x1 = fmaf(sv[c + 1], scale_log2, -m_ref);
-            float p0, p1;
-            if (poly_col(c)) {
-              // masked keys (-inf) must give exactly 0 like EX2; unmasked x is clamped into the poly's range
-              p0 = masked ? (x0 > -125.f ? exp2_poly(x0) : 0.f) : exp2_poly(fmaxf(x0, -125.f));
-              p1 = masked ? (x1 > -125.f ? exp2_poly(x1) : 0.f) : exp2_poly(fmaxf(x1, -125.f));
+              for (int c = cb * 32; c < cb * 32 + 32; c += 2) {
+                const float x0 = fmaf(sv[c], scale_log2, -m_ref), x1 = fmaf(sv[c + 1], scale_log2, -m_ref);
+                float p0, p1;
+                if (poly_col(c)) {
+                  // masked keys (-inf) must give exactly 0 like EX2; unmasked x is clamped into the poly's range
+                  p0 = masked ? (x0 > -125.f ? exp2_poly(x0) : 0.f) : exp2_poly(fmaxf(x0, -125.f));
+                  p1 = masked ? (x1 > -125.f ? exp2_poly(x1) : 0.f) : exp2_poly(fmaxf(x1, -125.f));
+                } else {
+                  p0 = ex2_approx(x0);
+                  p1 = ex2_approx(x1);
+                }
+                r8[(c >> 1) & 7] += p0 + p1;
+                pk[c / 2] = pack_bf16x2(p0, p1);
+              }
             } else {
-              p0 = ex2_approx(x0);
-              p1 = ex2_approx(x1);
+  #pragma unroll
+              for (int c = cb * 32; c < cb * 32 + 32; c += 2) pk[c / 2] = 0u;
             }
-            r8[(c >> 1) & 7] += p0 + p1;
-            pk[c / 2] = pack_bf16x2(p0, p1);
+          };
+          if constexpr (CAUSAL) {
+            exp_chunk(std::integral_constant<int, 0>{});
+            exp_chunk(std::integral_constant<int, 1>{});
+            exp_chunk(std::integral_constant<int, 2>{});
+            exp_chunk(std::integral_constant<int, 3>{});
+          } else {
+  #pragma unroll
+            for (int c = 0; c < TK; c += 2) {
+              const float x0 = fmaf(sv[c], scale_log2, -m_ref), x1 = fmaf(sv[c + 1], scale_log2, -m_ref);
+              float p0, p1;
+              if (poly_col(c)) {
+                // masked keys (-inf) must give exactly 0 like EX2; unmasked x is clamped into the poly's range
+                p0 = masked ? (x0 > -125.f ? exp2_poly(x0) : 0.f) : exp2_poly(fmaxf(x0, -125.f));
+                p1 = masked ? (x1 > -125.f ? exp2_poly(x1) : 0.f) : exp2_poly(fmaxf(x1, -125.f));
+              } else {
+                p0 = ex2_approx(x0);
+                p1 = ex2_approx(x1);
+              }
+              r8[(c >> 1) & 7] += p0 + p1;
+              pk[c / 2] = pack_bf16x2(p0, p1);
+            }
           }
           l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
           if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
@@ -579,11 +676,11 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
     const float scale_log2 = scale * 1.4426950408889634f;
     if (causal) {
       const int ugrid = L.n_units_max < max_grid ? L.n_units_max : max_grid;
-      return launch_pdl(attention_fwd_kernel<true>, dim3(ugrid > 0 ? ugrid : 1), dim3(kThreads), AttnSmem::kAlloc,
+      return launch_pdl(attention_fwd_kernel<true>, dim3(ugrid > 0 ? ugrid : 1), dim3(kThreadsOf<true>), AttnSmem::kAlloc,
                         stream, 1, tm, L.units, reinterpret_cast<const int2*>(L.unit_seq), L.n_units,
                         L.seq_of_tok, L.pos_in_seq, L.lengths, static_cast<__nv_bfloat16*>(o), d, scale_log2);
     }
-    return launch_pdl(attention_fwd_kernel<false>, dim3(grid), dim3(kThreads), AttnSmem::kAlloc, stream, 1, tm,
+    return launch_pdl(attention_fwd_kernel<false>, dim3(grid), dim3(kThreadsOf<false>), AttnSmem::kAlloc, stream, 1, tm,
                       L.tiles, reinterpret_cast<const int2*>(L.tile_seq), L.n_tiles, L.seq_of_tok, L.pos_in_seq,
                       L.lengths, static_cast<__nv_bfloat16*>(o), d, scale_log2);
   }
