@@ -493,6 +493,20 @@ def main():
             torch.cuda.synchronize()
             st_ms = float(np.mean(timed(g_stack.replay, n_stack)))
             what = "prelude(a1) once + 6 encoder layers, one CUDA graph"
+            # the same 6 layers cut into the gather groups the sharded stack uses at N > 1 (no communicator):
+            # the price of the group split that lets the gather overlap the compute
+            sh1 = ShardedStack(stack_params, n_groups=args.groups)
+            len_h1 = torch.tensor(loc_len, dtype=torch.int32)
+            y_sh1 = torch.empty_like(y_dev)
+            sh1(len_dev, len_h1, x_dev, out=y_sh1)
+            torch.cuda.synchronize()
+            g_sh1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_sh1):
+                sh1(len_dev, len_h1, x_dev, out=y_sh1)
+            for _ in range(args.warmup):
+                g_sh1.replay()
+            torch.cuda.synchronize()
+            grouped_ms = float(np.mean(timed(g_sh1.replay, n_stack)))
         else:
             # every rank: its sequences in `groups` window-aligned groups, each one layout through the 6
             # layers; group g's rows are gathered (NCCL, side stream) while group g + 1 computes
@@ -517,6 +531,11 @@ def main():
         stack = {"layers": 6, "ms_per_step": st_ms, "steps": n_stack,
                  "value": 6 * useful_flops(lengths, d, dff) / (st_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                  "step": what}
+        if world == 1:
+            stack["grouped"] = {"groups": args.groups, "ms_per_step": grouped_ms,
+                                "note": "cora_encoder_stack_sharded_fwd with one rank: the batch in window-aligned "
+                                        "groups, each one layout through the 6 layers (the N > 1 overlap schedule "
+                                        "without the gather)"}
 
     # ---------------------------------------------------------------- e2e: host buffers through the C ABI
     e2e = None
