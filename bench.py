@@ -10,7 +10,8 @@ metric is quoted on: bs 128, Wiki512-like lengths (configs[3], "C4").  Metric: u
 TFLOP/s = (2 T (4 d^2 + 2 d d_ff) + 4 d sum L^2) / step time; ms/step is reported beside it.
 
 Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the launching
-stream, with a 256 MB L2 flush between steps (outside the events); barrier + synchronize on both
+stream, with an L2 flush between steps (outside the events: 256 MB written, then 256 MB read so the flush's
+dirty lines are written back before the step starts); barrier + synchronize on both
 sides; the max over ranks.  `--impl reference` times the fp64 CPU oracle instead (the reference
 arm of this tier: a deliberately slow program).
 """
@@ -308,7 +309,16 @@ def main():
     x_full = torch.tensor(x_all, dtype=torch.float32).to(torch.bfloat16).to(dev)
     y_full = torch.empty(T_all, d, dtype=torch.bfloat16, device=dev)
     x_dev, y_dev = x_full[r0:r1], y_full[r0:r1]
+    # L2 flush between timed steps: write a 256 MB buffer (> the 126 MB L2), then read a second one, so the
+    # flush's own dirty lines are written back to HBM before the step's events -- the step starts with a
+    # cold L2 holding no line of its inputs and no dirty data of the flush
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.ones(32 << 20, dtype=torch.int64, device=dev)
+    flush_acc = torch.empty((), dtype=torch.int64, device=dev)
+
+    def flush_l2():
+        flush.zero_()
+        torch.sum(flush_rd, dim=0, out=flush_acc)
     stream = torch.cuda.current_stream()
 
     lay_holder = {}
@@ -383,7 +393,7 @@ def main():
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
         for i in range(n):
             if not args.no_flush:
-                flush.zero_()
+                flush_l2()
             evs[i][0].record(stream)
             run()
             evs[i][1].record(stream)
@@ -554,7 +564,7 @@ def main():
                   for _ in range(args.steps)]
             for i in range(args.steps):
                 if not args.no_flush:
-                    flush.zero_()
+                    flush_l2()
                 ev[i][0].record(stream)
                 hf(len_h, x_h, y_h)
                 ev[i][1].record(stream)
@@ -659,7 +669,8 @@ def main():
         "config": {"workload": args.config, "batch": int(len(lengths)), "total_tokens": int(lengths.sum()),
                    "sum_L2": int((lengths ** 2).sum()), "max_len": int(lengths.max()), "d_model": d, "heads": H,
                    "d_ff": dff, "parallelism": f"seq-shard{world}" if world > 1 else "single",
-                   "l2": "no flush" if args.no_flush else "flushed (256 MB write) between steps",
+                   "l2": "no flush" if args.no_flush else ("flushed between steps: 256 MB written, then 256 MB read "
+                                                            "(the flush's dirty lines leave L2 before the step)"),
                    "step": f"prelude(a1) + {layer_launches} layer kernels (a2..a8"
                    + (", LayerNorm fused into the out-proj / FF2 GEMM epilogues)" if fused_ln else ")") + (" per rank; NCCL all-gather timed separately (multi_gpu)" if world > 1 else ""),
                    "launch": "eager" if args.no_graph else "CUDA graph replay per step, programmatic dependent launch"},
