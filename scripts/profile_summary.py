@@ -27,7 +27,7 @@ STEP_ORDER_FUSED = ["prelude", "qkv_gemm", "attention", "out_proj_gemm+ln1", "ff
 
 def short(name: str) -> str:
     for key in ("layout_merged", "layout_scan", "fusion_maps", "gemm", "attention_fwd", "attention_simt", "layernorm",
-                "ragged_softmax", "FillFunctor", "vectorized_elementwise"):
+                "ragged_softmax", "FillFunctor", "vectorized_elementwise", "reduce_kernel", "reduce"):
         if key in name:
             return key
     return name[:40]
@@ -52,11 +52,14 @@ def launches(tag_dir):
     ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
     seq = [(short(r[ik]), float(r[iv]) / 1000.0) for r in rows[1:] if len(r) > iv]
     # keep our kernels of the LAST complete step (layout_scan starts a step)
-    ours = [(k, t) for k, t in seq if k not in ("FillFunctor", "vectorized_elementwise")]
+    ours = [(k, t) for k, t in seq if k not in ("FillFunctor", "vectorized_elementwise", "reduce_kernel", "reduce")]
     starts = [i for i, (k, _) in enumerate(ours) if k in ("layout_merged", "layout_scan")]
     if not starts:
         return None
+    # the last step that has all its kernels (the launch list may end with an incomplete one)
     last = ours[starts[-1]:]
+    if len(last) < len(STEP_ORDER_FUSED) and len(starts) > 1:
+        last = ours[starts[-2]:starts[-1]]
     # 5 layer kernels: LayerNorm fused into the out-proj / FF2 GEMM epilogues (d_model 512)
     order = STEP_ORDER_FUSED if len(last) == len(STEP_ORDER_FUSED) else STEP_ORDER
     last = last[:len(order)]
