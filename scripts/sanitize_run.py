@@ -35,9 +35,15 @@ for lengths, d, H, dff in ((list(synth.C1_LENGTHS), 16, 2, 32), ([3, 130, 1, 64,
     torch.cuda.synchronize()
     print("layer", lengths, float(y.float().abs().mean()), float(y2.float().abs().mean()), float(y3.float().abs().mean()),
           float(o.float().abs().mean()), float(ys.float().sum()), float(ln.float().abs().mean()), flush=True)
-dims = [(130, 264, 128), (64, 8, 64)]
-a = torch.randn(2, 130, 128, device="cuda").to(torch.bfloat16)
-b = torch.randn(2, 128, 264, device="cuda").to(torch.bfloat16)
+    # round 2: the sharded stack (gather groups, one rank), the causal kernel's chunk liveness
+    from paper_2110_10221_b200.dist import ShardedStack
+    y4 = ShardedStack([params, params], n_groups=3)(L, torch.tensor(lengths, dtype=torch.int32), x)
+    o2 = P.ragged_attention(lay, qkv, d // H)
+    torch.cuda.synchronize()
+    print("round2", float(y4.float().abs().mean()), float(o2.float().abs().mean()), flush=True)
+dims = [(130, 264, 128), (64, 8, 64), (64, 64, 0)]
+a = torch.randn(3, 130, 128, device="cuda").to(torch.bfloat16)
+b = torch.randn(3, 128, 264, device="cuda").to(torch.bfloat16)
 c = P.vgemm(a, b, dims)
 l = torch.randn(384, 384, device="cuda").to(torch.bfloat16)
 bb = torch.randn(384, 64, device="cuda").to(torch.bfloat16)
