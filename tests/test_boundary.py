@@ -115,3 +115,28 @@ def test_shard_entry_points_validate():
     p.d_model, p.heads, p.d_ff = 512, 8, 2048
     assert L.cora_encoder_stack_sharded_workspace_bytes(ctypes.byref(p), 0, 4, 16, 512) == 0
     assert L.cora_encoder_stack_sharded_workspace_bytes(ctypes.byref(p), 2, 4, 16, 512) > 0
+
+
+def test_vgemm_plan_host_logic():
+    """cora_vgemm_plan (host-only): sizes, validation, and the serialised work list (longest reduction first)."""
+    from paper_2110_10221_b200 import _lib as C
+    L = C.lib()
+    dims = [(300, 200, 256), (128, 264, 64), (0, 8, 64), (64, 64, 0)]
+    dh = (ctypes.c_int32 * 12)(*[v for r in dims for v in r])
+    n = L.cora_vgemm_plan_bytes(4, dh)
+    units = sum(-(-m // 128) * -(-nn // 256) for m, nn, _ in dims)
+    assert n == 16 + 16 * units + 8 * 4
+    assert L.cora_vgemm_workspace_bytes(4, dh) == n
+    buf = (ctypes.c_uint8 * n)()
+    assert L.cora_vgemm_plan(4, dh, 300, 264, 256, buf, n) == C.CORA_OK
+    h = np.frombuffer(bytes(buf), dtype=np.int32)
+    assert h[1] == 4 and h[2] == units
+    u = h[4:4 + 4 * units].reshape(units, 4)  # (problem, m0, n0, k-blocks)
+    assert list(u[:, 3]) == sorted(u[:, 3], reverse=True)  # longest reduction first
+    assert sorted(map(tuple, u[:, :3])) == sorted((p, m0, n0) for p, (m, nn, _k) in enumerate(dims)
+                                                  for m0 in range(0, m, 128) for n0 in range(0, nn, 256))
+    assert L.cora_vgemm_plan(4, dh, 300, 264, 256, buf, n - 1) == C.CORA_ERR_INVALID      # small buffer
+    assert L.cora_vgemm_plan(4, dh, 200, 264, 256, buf, n) == C.CORA_ERR_INVALID          # M_i > m_max
+    bad = (ctypes.c_int32 * 3)(64, 64, 100)
+    assert L.cora_vgemm_plan(1, bad, 64, 64, 128, buf, n) == C.CORA_ERR_UNSUPPORTED       # partial k-block
+    assert L.cora_vgemm_plan_bytes(1, (ctypes.c_int32 * 3)(-1, 8, 8)) == 0

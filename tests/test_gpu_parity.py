@@ -431,7 +431,7 @@ def test_layer_full_batch_against_oracle(cfg):
 
 
 @pytest.mark.parametrize("batch,hi", [(3, 200), (12, 300), (24, 400), (40, 512)])
-def test_layer_small_t_splitk(batch, hi):
+def test_layer_small_t(batch, hi):
     # small T (a few to ~20 256-row units for 33 four-CTA clusters: the fused GEMM + LN kernels run one
     # partial wave) against the oracle, whole batch or sampled
     lengths = synth.uniform_lengths(batch, 1, hi, seed=70 + batch)
