@@ -84,6 +84,27 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+
+#ifdef CORA_ATTN_TRACE
+// Phase trace (profiling builds only): softmax warp 0 lane 0 and the MMA thread of the first kTraceCtas
+// CTAs record (clock64 << 8 | event) into a per-CTA, per-role buffer of kTraceLen entries.
+constexpr int kTraceCtas = 296, kTraceLen = 2048;
+__device__ uint64_t g_attn_trace[kTraceCtas][2][kTraceLen];
+__device__ int g_attn_trace_n[kTraceCtas][2];
+#define ATR(role, ev)                                                                              \
+  do {                                                                                            \
+    if (blockIdx.x < kTraceCtas && atr_n < kTraceLen)                                             \
+      g_attn_trace[blockIdx.x][role][atr_n++] = (clock64() << 8) | (ev);                          \
+  } while (0)
+#define ATR_DONE(role) do { if (blockIdx.x < kTraceCtas) g_attn_trace_n[blockIdx.x][role] = atr_n; } while (0)
+#define ATR_SM(ev) do { if (qd == 0 && lane == 0) ATR(0, ev); } while (0)
+#define ATR_MMA(ev) ATR(1, ev)
+#else
+#define ATR_SM(ev) do {} while (0)
+#define ATR_MMA(ev) do {} while (0)
+#define ATR_DONE(role) do {} while (0)
+#endif
+
 struct AttnSmem {
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + QSTAGES * kTileBytes;
@@ -256,6 +277,9 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
+#ifdef CORA_ATTN_TRACE
+      int atr_n = 0;
+#endif
       constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK);
       constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HD, /*b_mn_major=*/true);
       int qs = 0, ks = 0, vs = 0;
@@ -269,8 +293,11 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           mbar_wait<false>(&q_full[qs], q_ph);
           const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
           auto issue_s = [&](bool last) {
+            ATR_MMA(20);
             mbar_wait<false>(&k_full[ks], k_ph);
+            ATR_MMA(21);
             mbar_wait<false>(s_empty, s_ph ^ 1);
+            ATR_MMA(22);
             s_ph ^= 1;
             tc_fence_after();
             const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
@@ -287,8 +314,10 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           for (int j = 0; j < nkv; ++j) {
             if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
             mbar_wait<false>(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
+            ATR_MMA(23);
             p_ph ^= 1;
             mbar_wait<false>(&v_full[vs], v_ph);
+            ATR_MMA(24);
             if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
               mbar_wait<false>(o_empty, o_ph ^ 1);
               o_ph ^= 1;
@@ -303,11 +332,13 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             }
             umma_commit(&v_empty[vs]);
             umma_commit(pv_done);
+            ATR_MMA(25);
             if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
           }
           if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
         }
       }
+      ATR_DONE(1);
     }
   }
   } else {
@@ -322,6 +353,9 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     const int i = qd * 32 + lane;  // query row within the tile
     const uint32_t t_lane = (qd * 32) << 16;
     uint32_t s_ph = 0, pv_ph = 0;
+#ifdef CORA_ATTN_TRACE
+    int atr_n = 0;
+#endif
     // the next tile's metadata is prefetched one tile ahead into shared memory with cp.async (no
     // registers held while in flight; prefetching into registers spilled)
     int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + qd * 2;  // [2 slots] per warp
@@ -380,6 +414,7 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           continue;
         }
         float m_ref = -INFINITY, l = 0.f;
+        ATR_SM(9);
         for (int j = 0; j < nkv; ++j) {
           const int valid = L - j * TK;  // keys of this tile that belong to sequence b (>= 1)
           const bool diag = CAUSAL && j == cur.qt;
@@ -394,13 +429,16 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             if (diag && live > static_cast<int>(qd) + 1) live = static_cast<int>(qd) + 1;
             if (cur.packed) live = TK / 32;
           }
+          ATR_SM(1);
           mbar_wait<false>(s_full, s_ph);
+          ATR_SM(2);
           s_ph ^= 1;
           tc_fence_after();
           uint32_t sr[TK];
   #pragma unroll
           for (int cb = 0; cb < TK / 32; ++cb) CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemS + cb * 32, (sr + cb * 32));
           tmem_ld_wait();
+          ATR_SM(3);
           // S is in registers: hand the TMEM buffer back so S_{j+1} runs under this softmax
           tc_fence_before();
           __syncwarp();
@@ -460,6 +498,7 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           }
           const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                  fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
+          ATR_SM(4);
           // lazy rescale: move the reference max only when it is exceeded by > kRescaleLog2
           const bool bump = mx > m_ref + kRescaleLog2;
           const float m_new = bump ? mx : m_ref;
@@ -516,12 +555,14 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
               pk[c / 2] = pack_bf16x2(p0, p1);
             }
           }
+          ATR_SM(5);
           l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
           if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
             mbar_wait<false>(pv_done, pv_ph);
             pv_ph ^= 1;
             tc_fence_after();
           }
+          ATR_SM(6);
           CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP, pk);
           CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP + 32, (pk + 32));
           // rescale the O accumulator in place when some row of this warp moved its reference max
@@ -541,9 +582,11 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
+          ATR_SM(7);
         }
         // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
         mbar_wait<false>(pv_done, pv_ph);
+        ATR_SM(8);
         pv_ph ^= 1;
         tc_fence_after();
         uint32_t orr[HD];
@@ -576,8 +619,10 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             }
           }
         }
+        ATR_SM(10);
       }
     }
+    if (qd == 0 && lane == 0) ATR_DONE(0);
   }
 
   tc_fence_before();
@@ -653,6 +698,15 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(const __nv_bfloat16
 
 }  // namespace
 
+#ifdef CORA_ATTN_TRACE
+extern "C" int cora_debug_attn_trace(void* dst, void* counts) {
+  cudaMemcpyFromSymbol(dst, g_attn_trace, sizeof(g_attn_trace));
+  cudaMemcpyFromSymbol(counts, g_attn_trace_n, sizeof(g_attn_trace_n));
+  static int z[kTraceCtas][2] = {};
+  return cudaMemcpyToSymbol(g_attn_trace_n, z, sizeof(z));
+}
+#endif
+
 cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, int32_t head_dim, float scale,
                              cudaStream_t stream, bool causal) {
   if (L.total_tokens == 0 || L.batch == 0) return cudaSuccess;
@@ -668,6 +722,7 @@ cudaError_t launch_attention(const cora_layout_t& L, const void* qkv, void* o, i
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem::kAlloc);
         if (e != cudaSuccess) return e;
       }
+
       attr_set[dev] = true;
     }
     const int max_grid = 2 * device_sm_count();

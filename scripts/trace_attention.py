@@ -24,10 +24,12 @@ from paper_2110_10221_b200 import _lib
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4-wiki512"
 causal = len(sys.argv) > 2 and sys.argv[2] == "causal"
-lengths, d, H, _ = synth.config(cfg)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+from attn_probe import lengths_of
+lengths, d, H = lengths_of(cfg), 512, 8
 T = int(lengths.sum())
 qkv = torch.randn(T, 3 * d, device="cuda").to(torch.bfloat16)
-lay = P.layout_build(torch.tensor(lengths, dtype=torch.int32, device="cuda"), T, H, 512)
+lay = P.layout_build(torch.tensor(lengths, dtype=torch.int32, device="cuda"), T, H, max(512, int(lengths.max())))
 o = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
 lib = ctypes.CDLL(_lib.LIB_PATH)
 NC, NL = 296, 2048
@@ -54,11 +56,24 @@ def phases(role, pairs):
             acc[(e0, e1)].append(t1 - t0)
     return acc, spans
 
-names = {9: "tile", 1: "pre-wait", 2: "S ready", 3: "S in regs", 4: "max", 5: "exps", 6: "PV done", 7: "P handed",
-         8: "last PV", 20: "issue_s", 21: "K ready", 22: "S free", 23: "P ready", 24: "V ready", 25: "PV issued", 10: "O in regs", 11: "loop top", 12: "meta", 13: "S released", 14: "masked", 26: "PV MMAs out", 27: "PV committed"}
+names = {36: "PV1 mma start", 37: "PV1 mma end", 3: "token", 31: "K1 ready", 33: "P1 ready", 35: "PV1 issued", 9: "tile", 1: "pre-wait", 2: "S ready", 3: "S in regs", 4: "max", 5: "exps", 6: "PV done", 7: "P handed",
+         8: "last PV", 20: "issue_s", 21: "K ready", 22: "S free", 23: "P ready", 24: "V ready", 25: "PV issued", 10: "O in regs", 11: "loop top", 12: "meta", 13: "S released", 14: "masked", 26: "PV mma start", 27: "PV mma end"}
 for role, title in ((0, "softmax warp 0"), (1, "MMA thread")):
     acc, spans = phases(role, None)
     print(f"== {title}: {len(spans)} CTAs, mean span {np.mean(spans):.0f} clk")
     tot = sum(sum(v) for v in acc.values())
     for (a, b), v in sorted(acc.items(), key=lambda t: -sum(t[1]))[:22]:
         print(f"  {names.get(a, a):>10} -> {names.get(b, b):<10} n={len(v):6d} mean {np.mean(v):7.0f} clk  share {sum(v) / tot:6.1%}")
+
+if os.environ.get("TIMELINE"):
+    # merged timeline of both roles of CTA c (same SM clock), steps s0..s0+n
+    c = int(os.environ.get("TL_CTA", "0"))
+    ev = []
+    for role in (0, 1):
+        n = int(cnt[c, role])
+        ev += [(int(x) >> 8, int(x) & 0xFF, role) for x in buf[c, role, :n]]
+    ev.sort()
+    t0 = ev[0][0]
+    lo, hi = int(os.environ.get("TL_FROM", "200")), int(os.environ.get("TL_TO", "260"))
+    for k, (t, e, role) in enumerate(ev[lo:hi]):
+        print(f"{t - t0:9d} {'  ' * 0 if role == 0 else ' ' * 40}{names.get(e, e)}")
