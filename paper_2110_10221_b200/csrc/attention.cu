@@ -369,7 +369,9 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     int slot = 0;
     prefetch_meta(blockIdx.x, 0);
     for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x, slot ^= 1) {
+      ATR_SM(11);
       cp_async_wait_all();
+      ATR_SM(12);
       __syncwarp();
       const int4 mt = meta[slot];
       __syncwarp();
@@ -493,6 +495,9 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             max_chunk(std::integral_constant<int, 2>{});
             max_chunk(std::integral_constant<int, 3>{});
           } else {
+#ifdef CORA_ATTN_PROF_MAX_FIRST_ONLY  // profiling build only: the row max of the first KV tile alone
+            if (j == 0)
+#endif
   #pragma unroll
             for (int c = 0; c < TK; ++c) m8[c & 7] = fmaxf(m8[c & 7], sv[c]);
           }
@@ -593,11 +598,16 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
         CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO, orr);
         CORA_TMEM_LD_32X32B_X32(tmem_base + t_lane + kTmemO + 32, (orr + 32));
         tmem_ld_wait();
+        ATR_SM(13);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(o_empty);
         const int qrow = cur.qt * TQ + i;
+#ifdef CORA_ATTN_PROF_NO_STORE  // profiling build only: O is not written
+        if (qrow < L && l == 12345.f) {
+#else
         if (qrow < L) {
+#endif
           const float inv = 1.f / l;
           __nv_bfloat16* orow = out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD;
           if (out_v8) {  // 32-B stores: one full sector per lane

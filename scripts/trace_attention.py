@@ -57,7 +57,7 @@ def phases(role, pairs):
     return acc, spans
 
 names = {36: "PV1 mma start", 37: "PV1 mma end", 3: "token", 31: "K1 ready", 33: "P1 ready", 35: "PV1 issued", 9: "tile", 1: "pre-wait", 2: "S ready", 3: "S in regs", 4: "max", 5: "exps", 6: "PV done", 7: "P handed",
-         8: "last PV", 20: "issue_s", 21: "K ready", 22: "S free", 23: "P ready", 24: "V ready", 25: "PV issued", 10: "O in regs", 11: "loop top", 12: "meta", 13: "S released", 14: "masked", 26: "PV mma start", 27: "PV mma end"}
+         8: "last PV", 20: "issue_s", 21: "K ready", 22: "S free", 23: "P ready", 24: "V ready", 25: "PV issued", 10: "O stored", 11: "loop top", 12: "meta ready", 13: "O in regs", 14: "masked", 26: "PV mma start", 27: "PV mma end"}
 for role, title in ((0, "softmax warp 0"), (1, "MMA thread")):
     acc, spans = phases(role, None)
     print(f"== {title}: {len(spans)} CTAs, mean span {np.mean(spans):.0f} clk")
