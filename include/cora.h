@@ -216,9 +216,14 @@ size_t cora_forward_host_workspace_bytes(const cora_encoder_params_t* p, int32_t
  * are copied in, computed and copied out as a pipeline over the caller's stream and two library-owned
  * side streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the layer on chunk c); each chunk is a
  * ragged batch of its own, so every row is computed as in the one-shot path (bitwise, except that
- * sequences of < 128 tokens may be packed into different attention windows).  The side streams
- * and events are created once per device; concurrent calls from several host threads on one device are
- * not supported.  The device status word is not read (no hidden sync): call cora_layout_status on
+ * sequences of < 128 tokens may be packed into different attention windows).  The pipelined work is
+ * captured once into a CUDA graph (on a library-owned stream) and replayed while every argument that
+ * shapes it is unchanged -- the parameter struct, the lengths' contents, the sizes, the host / workspace
+ * pointers and whether layout_out is given (a 64-bit hash of them); the contents of x_host are read at
+ * replay time.  A call with other arguments re-captures; a capture failure (e.g. pageable host memory)
+ * falls back to enqueueing directly; CORA_HOST_NO_GRAPH (environment) disables the graph.  The side
+ * streams, events and graph are kept once per device; concurrent calls from several host threads on one
+ * device are not supported.  The device status word is not read (no hidden sync): call cora_layout_status on
  * *layout_out (the whole batch's layout, built on `stream`) after synchronising to detect data errors
  * (invalid lengths also disable the chunking).  layout_out may be NULL (then no whole-batch layout is
  * built when chunking).  T = total_tokens must equal sum(lengths_host). */

@@ -524,9 +524,19 @@ namespace {
 // Side streams and events of the pipelined host forward, created once per device (never on the hot path
 // after the first call).
 constexpr int kMaxChunks = 16;
+// The host pipeline of one device: two side streams + fork/join events, a capture stream, and the CUDA
+// graph of the last call (re-used while the call's arguments are the same: its enqueue cost -- ~100 kernel
+// launches and copies at 16 chunks, ~0.8 ms of host time -- would otherwise bound the call).
+struct HostGraph {
+  uint64_t key = 0;  // hash of every argument that shapes the enqueued work (0: none cached)
+  cudaGraphExec_t exec = nullptr;
+  cora_layout_t layout{};
+  bool has_layout = false;
+};
 struct HostPipe {
-  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr, cap = nullptr;
   cudaEvent_t start = nullptr, done = nullptr, h2d_ev[kMaxChunks] = {}, comp_ev[kMaxChunks] = {};
+  HostGraph graph;
   bool ok = false;
 };
 HostPipe g_pipe[64];
@@ -540,6 +550,7 @@ HostPipe* host_pipe() {
   if (!hp.ok) {
     bool good = cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking) == cudaSuccess &&
                 cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&hp.cap, cudaStreamNonBlocking) == cudaSuccess &&
                 cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming) == cudaSuccess &&
                 cudaEventCreateWithFlags(&hp.done, cudaEventDisableTiming) == cudaSuccess;
     for (int c = 0; good && c < kMaxChunks; ++c)
@@ -550,39 +561,37 @@ HostPipe* host_pipe() {
   }
   return &hp;
 }
-}  // namespace
+#ifdef CORA_HOST_TRACE
+// Pipeline timeline (profiling builds only, with CORA_HOST_NO_GRAPH set): timing events after each chunk's
+// H2D, layer and D2H, read back by cora_debug_host_trace.
+struct HostTrace {
+  bool on = false, made = false;
+  int K = 0;
+  cudaEvent_t t0 = nullptr, h2d[kMaxChunks] = {}, comp[kMaxChunks] = {}, d2h[kMaxChunks] = {};
+};
+HostTrace g_htrace;
+void htrace_rec(cudaEvent_t* e, cudaStream_t st) {
+  if (!g_htrace.on) return;
+  if (*e == nullptr) cudaEventCreate(e);
+  cudaEventRecord(*e, st);
+}
+#define HTRACE(e, st) htrace_rec(&g_htrace.e, st)
+#else
+#define HTRACE(e, st) \
+  do {                \
+  } while (0)
+#endif
 
-cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
-                                        int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host,
-                                        void* ws, size_t ws_bytes, cora_layout_t* layout_out, void* stream) {
-  if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return CORA_ERR_INVALID;
-  if ((batch > 0 && lengths_host == nullptr) || ws == nullptr || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
-    return CORA_ERR_INVALID;
-  if (total_tokens > 0 && (x_host == nullptr || y_host == nullptr)) return CORA_ERR_INVALID;
-  const size_t need = cora_forward_host_workspace_bytes(p, batch, total_tokens, max_len);
-  if (need == 0 || ws_bytes < need) return CORA_ERR_INVALID;
-  const int32_t d = p->d_model;
-  const size_t xbytes = 2ull * static_cast<size_t>(total_tokens) * d;
-  const size_t xy = align_up(xbytes);
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  int32_t* d_len = reinterpret_cast<int32_t*>(w);
-  w += align_up(sizeof(int32_t) * (batch + 1));
-  uint8_t* d_x = w;
-  w += xy;
-  uint8_t* d_y = w;
-  w += xy;
-  const size_t lay_bytes = cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len);
-  void* lay_ws = w;  // the whole batch's layout (layout_out)
-  w += lay_bytes;
-  void* chunk_lay_ws = w;  // the current chunk's layout
-  w += lay_bytes;
-  const size_t layer_ws = ws_bytes - static_cast<size_t>(w - static_cast<uint8_t*>(ws));
-  cudaStream_t s = as_stream(stream);
+// FNV-1a over raw bytes (the graph-cache key)
+uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+  const uint8_t* b = static_cast<const uint8_t*>(data);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
 
-  // The lengths are on the host: chunk the batch there.  K contiguous sequence ranges of ~T/K tokens
-  // each are copied in, computed and copied out as a pipeline over three streams (H2D of chunk c+1 and
-  // D2H of chunk c-1 overlap the layer on chunk c; PCIe is full duplex): sequences are independent, so
-  // a chunk is a ragged batch of its own (its layout rebased to its first token).
+// Number of pipeline chunks for a batch (1 = one shot): the lengths are on the host, so the batch is cut
+// there; invalid lengths disable the chunking (the device status word reports them).
+int host_chunks(const int32_t* lengths_host, int32_t batch, int32_t total_tokens, int32_t max_len) {
   int64_t sum = 0;
   bool bad = false;
   for (int b = 0; b < batch; ++b) {
@@ -599,6 +608,35 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
     if (k >= 1 && k <= kMaxChunks && !bad && sum == total_tokens) K = k;
   }
   if (K > batch) K = batch > 0 ? batch : 1;
+  return K;
+}
+
+// Enqueue the whole host-buffer forward on stream `s` (the caller's, or the capture stream).
+cora_status_t host_forward_enqueue(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
+                                   int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host, void* ws,
+                                   size_t ws_bytes, cora_layout_t* layout_out, cudaStream_t s, int K, HostPipe* hp) {
+  void* stream = s;
+  const int32_t d = p->d_model;
+  const size_t xbytes = 2ull * static_cast<size_t>(total_tokens) * d;
+  const size_t xy = align_up(xbytes);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int32_t* d_len = reinterpret_cast<int32_t*>(w);
+  w += align_up(sizeof(int32_t) * (batch + 1));
+  uint8_t* d_x = w;
+  w += xy;
+  uint8_t* d_y = w;
+  w += xy;
+  const size_t lay_bytes = cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len);
+  void* lay_ws = w;  // the whole batch's layout (layout_out)
+  w += lay_bytes;
+  void* chunk_lay_ws = w;  // the current chunk's layout
+  w += lay_bytes;
+  const size_t layer_ws = ws_bytes - static_cast<size_t>(w - static_cast<uint8_t*>(ws));
+
+  // K contiguous sequence ranges of ~T/K tokens each are copied in, computed and copied out as a pipeline
+  // over three streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the layer on chunk c; PCIe is full
+  // duplex): sequences are independent, so a chunk is a ragged batch of its own (its layout rebased to its
+  // first token).
   int32_t seq_begin[kMaxChunks + 1], tok_begin[kMaxChunks + 1];
   seq_begin[0] = 0, tok_begin[0] = 0;
   {
@@ -611,7 +649,6 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
     }
     seq_begin[K] = batch, tok_begin[K] = total_tokens;
   }
-  HostPipe* hp = K > 1 ? host_pipe() : nullptr;
   if (hp == nullptr) K = 1, seq_begin[1] = batch, tok_begin[1] = total_tokens;
 
   if (batch > 0 && cudaMemcpyAsync(d_len, lengths_host, sizeof(int32_t) * batch, cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -633,6 +670,11 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
     }
   }
   // pipelined: fork the side streams off the caller's stream, join them back at the end
+#ifdef CORA_HOST_TRACE
+  g_htrace.on = true;
+  g_htrace.K = K;
+#endif
+  HTRACE(t0, s);
   if (cudaEventRecord(hp->start, s) != cudaSuccess || cudaStreamWaitEvent(hp->h2d, hp->start, 0) != cudaSuccess ||
       cudaStreamWaitEvent(hp->d2h, hp->start, 0) != cudaSuccess)
     return CORA_ERR_CUDA;
@@ -643,6 +685,7 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
                                      cudaMemcpyHostToDevice, hp->h2d) != cudaSuccess)
       return CORA_ERR_CUDA;
     if (cudaEventRecord(hp->h2d_ev[c], hp->h2d) != cudaSuccess) return CORA_ERR_CUDA;
+    HTRACE(h2d[c], hp->h2d);
   }
   for (int c = 0; c < K; ++c) {
     const int32_t nb = seq_begin[c + 1] - seq_begin[c], nt = tok_begin[c + 1] - tok_begin[c];
@@ -657,14 +700,97 @@ cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const in
       if (st != CORA_OK) return st;
     }
     if (cudaEventRecord(hp->comp_ev[c], s) != cudaSuccess) return CORA_ERR_CUDA;
+    HTRACE(comp[c], s);
     if (cudaStreamWaitEvent(hp->d2h, hp->comp_ev[c], 0) != cudaSuccess) return CORA_ERR_CUDA;
     const size_t off = row * tok_begin[c], bytes = row * nt;
     if (bytes > 0 && cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + off, d_y + off, bytes, cudaMemcpyDeviceToHost,
                                      hp->d2h) != cudaSuccess)
       return CORA_ERR_CUDA;
+    HTRACE(d2h[c], hp->d2h);
   }
   if (cudaEventRecord(hp->done, hp->d2h) != cudaSuccess || cudaStreamWaitEvent(s, hp->done, 0) != cudaSuccess)
     return CORA_ERR_CUDA;
+  return CORA_OK;
+}
+}  // namespace
+
+#ifdef CORA_HOST_TRACE
+// profiling: ms from the pipeline start to each chunk's H2D / layer / D2H completion (3 x K values)
+extern "C" int cora_debug_host_trace(float* out, int max_chunks) {
+  if (!g_htrace.on || g_htrace.t0 == nullptr) return 0;
+  const int K = g_htrace.K < max_chunks ? g_htrace.K : max_chunks;
+  cudaDeviceSynchronize();
+  for (int c = 0; c < K; ++c) {
+    cudaEventElapsedTime(&out[c], g_htrace.t0, g_htrace.h2d[c]);
+    cudaEventElapsedTime(&out[K + c], g_htrace.t0, g_htrace.comp[c]);
+    cudaEventElapsedTime(&out[2 * K + c], g_htrace.t0, g_htrace.d2h[c]);
+  }
+  return K;
+}
+#endif
+
+cora_status_t cora_encoder_forward_host(const cora_encoder_params_t* p, const int32_t* lengths_host, int32_t batch,
+                                        int32_t total_tokens, int32_t max_len, const void* x_host, void* y_host,
+                                        void* ws, size_t ws_bytes, cora_layout_t* layout_out, void* stream) {
+  if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return CORA_ERR_INVALID;
+  if ((batch > 0 && lengths_host == nullptr) || ws == nullptr || (reinterpret_cast<uintptr_t>(ws) % kAlign) != 0)
+    return CORA_ERR_INVALID;
+  if (total_tokens > 0 && (x_host == nullptr || y_host == nullptr)) return CORA_ERR_INVALID;
+  const size_t need = cora_forward_host_workspace_bytes(p, batch, total_tokens, max_len);
+  if (need == 0 || ws_bytes < need) return CORA_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  int K = host_chunks(lengths_host, batch, total_tokens, max_len);
+  HostPipe* hp = K > 1 ? host_pipe() : nullptr;
+  if (hp == nullptr) K = 1;
+  if (K == 1 || getenv("CORA_HOST_NO_GRAPH") != nullptr)
+    return host_forward_enqueue(p, lengths_host, batch, total_tokens, max_len, x_host, y_host, ws, ws_bytes,
+                                layout_out, s, K, hp);
+  // Pipelined calls replay a CUDA graph of the enqueued work, captured on the library's capture stream
+  // (the caller's stream may be the legacy default stream, which cannot be captured) and launched on the
+  // caller's stream.  The key covers every argument the enqueue depends on: the parameter struct (weight
+  // pointers, dims, activation, eps), the lengths, the sizes, the host and workspace pointers, the chunk
+  // count and whether a whole-batch layout is wanted.
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint64_t key = 1469598103934665603ull;
+  key = fnv1a(key, p, sizeof(*p));
+  key = fnv1a(key, lengths_host, sizeof(int32_t) * static_cast<size_t>(batch));
+  const int64_t scal[5] = {batch, total_tokens, max_len, K, layout_out != nullptr};
+  const void* ptrs[3] = {x_host, y_host, ws};
+  key = fnv1a(key, scal, sizeof(scal));
+  key = fnv1a(key, ptrs, sizeof(ptrs));
+  key = fnv1a(key, &ws_bytes, sizeof(ws_bytes));
+  key = fnv1a(key, &dev, sizeof(dev));
+  key |= 1;  // 0 means "nothing cached"
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  HostGraph& g = hp->graph;
+  if (g.key != key) {
+    if (g.exec != nullptr) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr, g.key = 0;
+    cora_layout_t lay{};
+    if (cudaStreamBeginCapture(hp->cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return CORA_ERR_CUDA;
+    const cora_status_t st = host_forward_enqueue(p, lengths_host, batch, total_tokens, max_len, x_host, y_host, ws,
+                                                  ws_bytes, layout_out != nullptr ? &lay : nullptr, hp->cap, K, hp);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(hp->cap, &graph);
+    if (st != CORA_OK || ce != cudaSuccess || graph == nullptr) {
+      if (graph != nullptr) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      // not capturable here (e.g. pageable host buffers): enqueue directly
+      return st != CORA_OK ? st
+                           : host_forward_enqueue(p, lengths_host, batch, total_tokens, max_len, x_host, y_host, ws,
+                                                  ws_bytes, layout_out, s, K, hp);
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      g.exec = nullptr;
+      return CORA_ERR_CUDA;
+    }
+    g.key = key, g.layout = lay, g.has_layout = layout_out != nullptr;
+  }
+  if (cudaGraphLaunch(g.exec, s) != cudaSuccess) return CORA_ERR_CUDA;
+  if (layout_out != nullptr && g.has_layout) *layout_out = g.layout;
   return CORA_OK;
 }
 

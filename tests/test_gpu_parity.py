@@ -5,6 +5,8 @@ bit-exact; bf16 tensor-core outputs max relative error <= 2e-2; fp32 elementwise
 """
 import math
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -611,6 +613,40 @@ def test_forward_host_matches_device_path(lengths):
     b = int(np.argmax(lengths))
     assert rel_err(y_h[ro[b]:ro[b + 1]].double().numpy(),
                    oracle.encoder_layer(x[ro[b]:ro[b + 1]], [lengths[b]], w)) <= TOL_BF16
+
+
+@pytest.mark.gpu
+def test_forward_host_graph_replay_and_recapture():
+    """Pipelined cora_encoder_forward_host calls replay a cached CUDA graph while the arguments are the same
+    (new x contents are copied at replay time) and re-capture when the lengths change."""
+    d, H, dff = 512, 8, 2048
+    w = synth.encoder_weights(d, H, dff)
+    params = P().EncoderParams.from_host(w)
+    la = list(synth.config("C3")[0])                                  # T >= 8192: 4 pipeline chunks
+    lb = list(np.roll(np.asarray(la), 7))                             # same T, other chunk cuts
+    T = int(np.sum(la))
+    assert T >= 8192 and int(np.sum(lb)) == T
+    hf = P().HostForward(params, len(la), T, 512)
+    y_h = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
+    for lengths, seed in ((la, 1), (la, 2), (lb, 3), (la, 4)):
+        x = synth.activations(T, d, seed=seed)
+        len_h = torch.tensor(np.asarray(lengths, np.int32)).pin_memory()
+        x_h = torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).pin_memory()
+        y_h.fill_(float("nan"))
+        hf(len_h, x_h, y_h)
+        torch.cuda.synchronize()
+        assert hf.status() == 0
+        y_graph = y_h.clone()
+        os.environ["CORA_HOST_NO_GRAPH"] = "1"  # the same chunked pipeline enqueued directly
+        try:
+            y_h.fill_(float("nan"))
+            hf(len_h, x_h, y_h)
+            torch.cuda.synchronize()
+        finally:
+            del os.environ["CORA_HOST_NO_GRAPH"]
+        assert torch.equal(y_graph, y_h), f"seed {seed}"
+        ref = P().encoder_layer(bf16_cuda(x), _layout(lengths, H), params).cpu()
+        assert rel_err(y_graph.float().numpy(), ref.float().numpy()) <= 1e-2  # windows may differ (f4-r1)
 
 
 # ---------------------------------------------------------------- prelude + layer in one call
