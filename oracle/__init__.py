@@ -17,7 +17,9 @@ Pins (tests/test_oracle_*.py, run with `-m "not gpu"`):
                 brute-force enumeration bijection, B.2 identities.
   tile list  -- brute-force sort of all (b,h,qt) by the stated key.
   attention  -- torch SDPA fp64 (B=1 reduces to textbook SDPA); padded+masked
-                dense brute force; invariants (rows sum to 1, L=1 -> O=V).
+                dense brute force; invariants (rows sum to 1, L=1 -> O=V);
+                the row-at-a-time form (long sequences) against torch SDPA
+                per sampled row, bidirectional and causal.
   softmax    -- SPEC example [0,0] -> [0.5,0.5]; shift invariance; sums.
   layernorm  -- torch.nn.functional.layer_norm fp64; closed-form moments.
   linear     -- pure-Python MAC loops on tiny inputs.
@@ -54,6 +56,7 @@ from .encoder import (  # noqa: F401
     softmax_row,
     ragged_softmax,
     ragged_attention,
+    ragged_attention_rows,
     attention_scores_ragged,
     encoder_layer,
     relu,

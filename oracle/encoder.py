@@ -149,6 +149,33 @@ def ragged_attention(qkv: np.ndarray, lengths: Sequence[int], heads: int, causal
     return out
 
 
+def ragged_attention_rows(qkv: np.ndarray, lengths: Sequence[int], heads: int, rows: Sequence[int],
+                          causal: bool = False) -> np.ndarray:
+    """The rows `rows` (packed token indices) of ragged_attention, one at a time: for token t of sequence b
+    (position i), O[t, h] = softmax_j(q_t . k_j / sqrt(d_h)) v_j over the keys j < L_b of its own sequence
+    (j <= i when causal) -- the same definition, for sequences too long to
+    form their L x L score matrices (max_len 16383).  Returns [len(rows), d]."""
+    T, three_d = qkv.shape
+    d = three_d // 3
+    dh = d // heads
+    row_off = row_offsets(lengths)
+    out = np.zeros((len(rows), d), np.float64)
+    for n, t in enumerate(rows):
+        b = int(np.searchsorted(row_off, t, side="right")) - 1
+        while int(lengths[b]) == 0:  # zero-length sequences share their row offset with the next one
+            b += 1
+        r0, L = row_off[b], int(lengths[b])
+        i = t - r0
+        nk = i + 1 if causal else L
+        for h in range(heads):
+            q = qkv[t, h * dh:(h + 1) * dh]
+            k = qkv[r0:r0 + nk, d + h * dh:d + (h + 1) * dh]
+            v = qkv[r0:r0 + nk, 2 * d + h * dh:2 * d + (h + 1) * dh]
+            p = softmax_row((k @ q) * (1.0 / math.sqrt(dh)))
+            out[n, h * dh:(h + 1) * dh] = p @ v
+    return out
+
+
 def encoder_layer(x: np.ndarray, lengths: Sequence[int], w, eps: float = 1e-5, act: str = "relu",
                   return_intermediates: bool = False):
     """Forward pass of one post-LN encoder layer over a ragged batch, fp64.

@@ -13,7 +13,7 @@ import torch
 
 import oracle
 import synth
-from util import TOL_BF16, TOL_F32, bf16_cuda, f32_cuda, rel_err, to_np
+from util import TOL_BF16, TOL_F32, bf16_cuda, f32_cuda, rel_err, rel_err_rows, to_np
 
 pytestmark = pytest.mark.gpu
 
@@ -349,6 +349,37 @@ def test_ragged_masked_attention(lengths, head_dim, heads):
     lay = _layout(lengths, heads)
     o = P().ragged_attention(lay, bf16_cuda(qkv), head_dim, causal=True)
     assert rel_err(to_np(o), oracle.ragged_attention(qkv, lengths, heads, causal=True)) <= TOL_BF16
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_long_sequences(causal):
+    """Sequences far beyond the paper's 512 tokens (33 q-tiles, a ragged last tile), with short and empty
+    neighbours: every row against the fp64 oracle."""
+    lengths, H, hd = [4097, 0, 130, 1, 2000], 8, 64
+    d = H * hd
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 41))
+    lay = _layout(lengths, H, max_len=4097)
+    o = P().ragged_attention(lay, bf16_cuda(qkv), hd, causal=causal)
+    assert rel_err_rows(to_np(o), oracle.ragged_attention(qkv, lengths, H, causal=causal)) <= TOL_BF16
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_max_len_sampled_rows(causal):
+    """The longest sequence the layout admits (max_len 16383: 128 q-tiles, the tile word's 7-bit q-tile field
+    at its limit) in a batch with short sequences, on sampled rows (every q-tile's first and last row, the
+    ragged tail, the neighbours) against the oracle's row-at-a-time form."""
+    lengths, H, hd = [3, 16383, 77], 2, 64
+    d = H * hd
+    qkv = synth.round_bf16(synth.normal((sum(lengths), 3 * d), 43))
+    lay = _layout(lengths, H, max_len=16383)
+    o = to_np(P().ragged_attention(lay, bf16_cuda(qkv), hd, causal=causal))
+    r0 = 3
+    rows = [0, 2] + [r0 + 128 * q for q in range(0, 128, 9)] + [r0 + 128 * q + 127 for q in range(0, 127, 13)]
+    rows += [r0 + 16382, r0 + 16383, r0 + 16383 + 76]
+    ref = oracle.ragged_attention_rows(qkv, lengths, H, rows, causal=causal)
+    assert rel_err_rows(o[rows], ref) <= TOL_BF16
 
 
 def _rescale_qkv(lengths, H, hd, seed):

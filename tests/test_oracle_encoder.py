@@ -225,3 +225,22 @@ def test_causal_attention_invariants():
     assert np.array_equal(out[:ro[2] + 4], out2[:ro[2] + 4])
     # FLOP count of the lower triangle
     assert oracle.causal_attention_flops([3], 8) == 4 * 8 * 6
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_rows_vs_torch_sdpa(causal):
+    """ragged_attention_rows (the row-at-a-time form for sequences too long for an L x L score matrix) against
+    torch SDPA fp64 per sequence (is_causal for the masked variant), on sampled rows of a batch with zero-length
+    sequences, a 1-token sequence and a sequence of 700 tokens (6 q-tiles)."""
+    lengths, H, d = [0, 700, 1, 0, 130, 5], 4, 64
+    qkv = _qkv(lengths, d, seed=11)
+    ro = oracle.row_offsets(lengths)
+    rows = [0, 1, 127, 128, 511, 699, 700, 701, 790, 830, 831, 835]
+    got = oracle.ragged_attention_rows(qkv, lengths, H, rows, causal=causal)
+    for n, t in enumerate(rows):
+        b = max(i for i in range(len(lengths)) if ro[i] <= t and lengths[i] > 0)
+        L, r0 = lengths[b], ro[b]
+        seq = qkv[r0:r0 + L]
+        q, k, v = (_t(seq[:, i * d:(i + 1) * d]).reshape(L, H, d // H).transpose(0, 1) for i in range(3))
+        ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal).transpose(0, 1).reshape(L, d)
+        assert np.abs(got[n] - ref[t - r0].numpy()).max() < 1e-13, (t, causal)
