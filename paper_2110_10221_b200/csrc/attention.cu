@@ -16,6 +16,8 @@
 //                  S_j = Q K_j^T  (M128 N128 K64, SS form, fp32 in TMEM cols [0,128))
 //                  O  += P_j V_j  (M128 N64 K128, TS form: P read from TMEM cols [128,192) as bf16
 //                                  pairs, V an MN-major smem operand; O in TMEM cols [192,256))
+//                the S MMAs run one KV step ahead of the PV MMAs over the CTA's whole work list, so the
+//                next tile's S_0 is issued before this tile's last PV
 //   warps 2..5 : softmax / correction / epilogue, one query row per thread (TMEM lane = row):
 //                  S_j is read from TMEM in one pass and the buffer released at once (so S_{j+1}
 //                  overlaps the exponentials), online softmax in the exp2 domain with a lazily
@@ -282,43 +284,70 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
 #endif
       constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK);
       constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HD, /*b_mn_major=*/true);
-      int qs = 0, ks = 0, vs = 0;
-      uint32_t q_ph = 0, k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
+      int ks = 0, vs = 0;
+      uint32_t k_ph = 0, v_ph = 0, s_ph = 0, p_ph = 0, o_ph = 0;
+      // The S iterator walks the flattened (tile, KV step) sequence one step ahead of the PV loop, across
+      // tile boundaries: the next tile's S_0 is issued before this tile's last PV, so the softmax warps find
+      // it ready when they finish the tile (their epilogue of the tile is deferred into the next one).
+      int s_idx = blockIdx.x, s_sub = 0, s_j = 0, s_nkv = 0, s_qs = 0;
+      uint32_t s_qph = 0;
+      WorkUnit s_wu{}, s_wu_next{};
+      auto tile_nkv = [](const WorkTile& t) {
+        return CAUSAL ? min((t.L + TK - 1) / TK, t.qt + 1) : (t.L + TK - 1) / TK;
+      };
+      if (s_idx < n_tiles) {
+        s_wu = wu_next;
+        s_nkv = tile_nkv(s_wu.tile(0));
+        if (s_idx + static_cast<int>(gridDim.x) < n_tiles)
+          s_wu_next = load_work<CAUSAL>(tiles, tile_seq, s_idx + gridDim.x);
+      }
+      auto issue_next_s = [&]() {
+        if (s_idx >= n_tiles) return;
+        ATR_MMA(20);
+        if (s_j == 0) mbar_wait<false>(&q_full[s_qs], s_qph);
+        mbar_wait<false>(&k_full[ks], k_ph);
+        ATR_MMA(21);
+        mbar_wait<false>(s_empty, s_ph ^ 1);  // the softmax has read the previous S
+        ATR_MMA(22);
+        s_ph ^= 1;
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + s_qs * kTileBytes);
+        const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
+  #pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
+                       make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
+        umma_commit(&k_empty[ks]);
+        umma_commit(s_full);
+        if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
+        if (++s_j == s_nkv) {  // the tile's last S: its Q slot is free once that MMA is done
+          umma_commit(&q_empty[s_qs]);
+          if (++s_qs == QSTAGES) s_qs = 0, s_qph ^= 1;
+          s_j = 0;
+          if (++s_sub == s_wu.count) {
+            s_sub = 0;
+            s_idx += gridDim.x;
+            s_wu = s_wu_next;
+            if (s_idx + static_cast<int>(gridDim.x) < n_tiles)
+              s_wu_next = load_work<CAUSAL>(tiles, tile_seq, s_idx + gridDim.x);
+          }
+          if (s_idx < n_tiles) s_nkv = tile_nkv(s_wu.tile(s_sub));
+        }
+      };
+      issue_next_s();
       for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
         const WorkUnit wu = wu_next;
         if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
         for (int sub = 0; sub < wu.count; ++sub) {
-          const WorkTile cur = wu.tile(sub);
-          const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
-          mbar_wait<false>(&q_full[qs], q_ph);
-          const uint32_t q_addr = smem_u32(smem + AttnSmem::kOffQ + qs * kTileBytes);
-          auto issue_s = [&](bool last) {
-            ATR_MMA(20);
-            mbar_wait<false>(&k_full[ks], k_ph);
-            ATR_MMA(21);
-            mbar_wait<false>(s_empty, s_ph ^ 1);
-            ATR_MMA(22);
-            s_ph ^= 1;
-            tc_fence_after();
-            const uint32_t k_addr = smem_u32(smem + AttnSmem::kOffK + ks * kTileBytes);
-  #pragma unroll
-            for (int k = 0; k < HD / 16; ++k)
-              umma_bf16_ss(tmem_base + kTmemS, make_sdesc_sw128(q_addr + k * 32, 16, 1024),
-                           make_sdesc_sw128(k_addr + k * 32, 16, 1024), idesc_s, k != 0);
-            umma_commit(&k_empty[ks]);
-            umma_commit(s_full);
-            if (last) umma_commit(&q_empty[qs]);  // Q slot free once the last S of the tile is done
-            if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
-          };
-          issue_s(nkv == 1);
+          const int nkv = tile_nkv(wu.tile(sub));
           for (int j = 0; j < nkv; ++j) {
-            if (j + 1 < nkv) issue_s(j + 2 == nkv);  // S_{j+1} overlaps the softmax of S_j
-            mbar_wait<false>(p_full, p_ph);                  // P_j in TMEM (and O rescaled if needed)
+            issue_next_s();                        // S_{k+1} overlaps the softmax of S_k
+            mbar_wait<false>(p_full, p_ph);        // P_j in TMEM (and O rescaled if needed)
             ATR_MMA(23);
             p_ph ^= 1;
             mbar_wait<false>(&v_full[vs], v_ph);
             ATR_MMA(24);
-            if (j == 0) {  // the previous tile's epilogue has read O out of TMEM
+            if (j == 0) {  // the softmax warps have read the previous tile's O out of TMEM
               mbar_wait<false>(o_empty, o_ph ^ 1);
               o_ph ^= 1;
             }
@@ -335,7 +364,6 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             ATR_MMA(25);
             if (++vs == VSTAGES) vs = 0, v_ph ^= 1;
           }
-          if (++qs == QSTAGES) qs = 0, q_ph ^= 1;
         }
       }
       ATR_DONE(1);
