@@ -40,6 +40,8 @@
 #include "cora_internal.h"
 #include "ptx.cuh"
 
+CORA_KSPAN_DEFINE(attn)
+
 namespace cora {
 namespace {
 
@@ -86,6 +88,15 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// 1 / x on the FMA pipe for normal x > 0 (the row sums l >= 2^-8): the bit-trick seed (relative error
+// < 1/8) and three Newton steps r <- r (2 - x r) (error squares each step: < 6e-8).  Keeps the tile
+// epilogue off MUFU, where a lone RCP queues behind the other CTA's exponentials.
+__device__ __forceinline__ float rcp_fma(float x) {
+  float r = __int_as_float(0x7EF311C3 - __float_as_int(x));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) r = fmaf(r, fmaf(-x, r, 1.f), r);
+  return r;
+}
 
 #ifdef CORA_ATTN_TRACE
 // Phase trace (profiling builds only): softmax warp 0 lane 0 and the MMA thread of the first kTraceCtas
@@ -166,6 +177,7 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
                          float scale_log2) {
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  KSPAN_ENTRY(attn, 1);
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::kOffBar);
@@ -216,6 +228,7 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
   WorkUnit wu_next{};
   if constexpr (!CAUSAL) tmem_base = *tmem_ptr;
   pdl_wait();  // QKV (previous kernel) complete and visible
+  KSPAN_WAITED(attn, 1);
   pdl_trigger();
   if constexpr (!CAUSAL) {
     n_tiles = *n_tiles_ptr;
@@ -636,7 +649,7 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
 #else
         if (qrow < L) {
 #endif
-          const float inv = 1.f / l;
+          const float inv = rcp_fma(l);
           __nv_bfloat16* orow = out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD;
           if (out_v8) {  // 32-B stores: one full sector per lane
   #pragma unroll
@@ -666,6 +679,7 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  KSPAN_EXIT(attn, 1);
 }
 
 // ---------------------------------------------------------------- SIMT kernel for other head dims

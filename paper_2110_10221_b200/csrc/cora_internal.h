@@ -8,6 +8,43 @@
 
 #include "../../include/cora.h"
 
+// Kernel spans (profiling builds only, -DCORA_KSPAN): per kernel slot, %globaltimer of the first CTA entry,
+// the last CTA exit and the first / last return from griddepcontrol.wait, collected with 64-bit atomics.
+// Slots: 0 prelude, 1 attention, 2 QKV, 3 out-proj + LN1, 4 FF1, 5 FF2 + LN2.  Each translation unit owns
+// its array (no relocatable device code) and exports cora_debug_kspan_<tu>(host[8][4], reset).
+#ifdef CORA_KSPAN
+__device__ __forceinline__ unsigned long long kspan_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CORA_KSPAN_DEFINE(tu)                                                                            \
+  __device__ unsigned long long g_kspan_##tu[8][4];                                                      \
+  extern "C" int cora_debug_kspan_##tu(unsigned long long* host, int reset) {                           \
+    if (reset) {                                                                                         \
+      unsigned long long init[8][4];                                                                     \
+      for (int i = 0; i < 8; ++i) init[i][0] = init[i][3] = ~0ull, init[i][1] = init[i][2] = 0ull;      \
+      return cudaMemcpyToSymbol(g_kspan_##tu, init, sizeof(init)) == cudaSuccess ? 0 : 1;               \
+    }                                                                                                    \
+    return cudaMemcpyFromSymbol(host, g_kspan_##tu, sizeof(g_kspan_##tu)) == cudaSuccess ? 0 : 1;       \
+  }
+#define KSPAN_ENTRY(tu, slot) do { if (threadIdx.x == 0) atomicMin(&g_kspan_##tu[slot][0], kspan_now()); } while (0)
+#define KSPAN_EXIT(tu, slot) do { if (threadIdx.x == 0) atomicMax(&g_kspan_##tu[slot][1], kspan_now()); } while (0)
+#define KSPAN_WAITED(tu, slot)                                                                           \
+  do {                                                                                                   \
+    if (threadIdx.x == 0) {                                                                              \
+      const unsigned long long t_ = kspan_now();                                                         \
+      atomicMax(&g_kspan_##tu[slot][2], t_);                                                             \
+      atomicMin(&g_kspan_##tu[slot][3], t_);                                                             \
+    }                                                                                                    \
+  } while (0)
+#else
+#define CORA_KSPAN_DEFINE(tu)
+#define KSPAN_ENTRY(tu, slot) ((void)0)
+#define KSPAN_EXIT(tu, slot) ((void)0)
+#define KSPAN_WAITED(tu, slot) ((void)0)
+#endif
+
 namespace cora {
 
 constexpr int kAttnHeadDim = 64;  // head_dim of the tcgen05 attention kernel

@@ -57,6 +57,8 @@ extern "C" int cora_debug_gemm_trace(unsigned long long* host, int n) {
 #define GTRACE(k) ((void)0)
 #endif
 
+CORA_KSPAN_DEFINE(gemm)
+
 namespace cora {
 namespace {
 
@@ -82,7 +84,9 @@ struct GemmSmem {
   static constexpr int kWarpCols = BN * 4 / EW;       // columns per epilogue warp
   static constexpr int kBufs = kWarpCols / BK;        // staging buffers per epilogue warp (one per chunk)
   static constexpr int kABytes = BM * BK * 2;         // this CTA's A rows
-  static constexpr int kBBytes = (CL > 1 ? BN / 2 : BN) * BK * 2;  // this CTA's share of the B tile
+  // this CTA's share of the B tile: half of it in a CTA pair (cta_group::2); all of it for one CTA or a
+  // DUO (LN with CL = 2: two single CTAs holding the two column halves of the same 128 rows)
+  static constexpr int kBBytes = ((CL == 4 || (CL == 2 && !LN)) ? BN / 2 : BN) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + STAGES * kABytes;
@@ -135,6 +139,10 @@ __device__ __forceinline__ float apply_act(float x, int act) {
 // (cta_group::2), pair rank r owning rows [128 r, 128 r + 128) of it; 4 (LN only) = two CTA pairs compute
 // the two BN-column halves of the same 256 rows (N = 2 BN), so every row of the output lives in one
 // cluster and its LayerNorm statistics are combined across the pairs (section "LN epilogue" below).
+// DUO (LN with CL = 2): two single CTAs (cta_group::1) of a 2-CTA cluster compute the two BN-column halves
+// of the same 128 rows, so the LN GEMM tiles all 148 SMs (clusters of 4 strand 16 at GPC boundaries) in
+// units of half the rows; each CTA's epilogue is the pair CTA's (the same 128 x BN accumulator and row
+// segments), only the statistics partner differs (rank ^ 1 instead of rank ^ 2).
 template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN, bool LNREG, int ACT>
 __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
   // staged LN), or the row segment lives in registers (LNREG) / there is no residual: one reused buffer
   constexpr int EW = epi_warps<LN, LNREG>();
   using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? BN * 4 / EW / BK : (LNREG ? 0 : 1), EW>;
-  static_assert(!LN || (CL == 4 && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs with a residual");
+  static_assert(!LN || ((CL == 4 || CL == 2) && RESIDUAL), "the LayerNorm epilogue runs on 2 CTA pairs or a DUO with a residual");
   // SWIZZLE_128B atoms need 1024-B alignment; the dynamic smem window is declared so aligned
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -160,6 +168,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
   uint64_t* xch_bar = res_bar + EW * S::kBufs;  // [2 acc] partner's row partials landed (LN)
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(xch_bar + 2);
   if (threadIdx.x == 0) GTRACE(0);
+  constexpr int kSpanSlot = LN ? (LNREG ? 5 : 3) : (ACT != CORA_ACT_NONE ? 4 : 2);
+  KSPAN_ENTRY(gemm, kSpanSlot);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int m_blocks = (M + BM - 1) / BM;
@@ -167,14 +177,17 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
   const int k_blocks = (K + BK - 1) / BK;
   // work units: 128-row tiles (CL = 1), 256-row tiles of one BN-column block (CL = 2) or 256 full rows
   // (CL = 4), strided over CTAs / clusters
-  constexpr bool PAIR = CL > 1;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  constexpr bool DUO = LN && CL == 2;        // two single CTAs (cta_group::1), one per column half
+  constexpr bool PAIR = CL > 1 && !DUO;      // cta_group::2 CTA pairs
+  constexpr bool CLUSTER = CL > 1;
+  const uint32_t rank = CLUSTER ? cluster_ctarank() : 0u;
   const uint32_t prank = PAIR ? (rank & 1u) : 0u;       // rank inside the CTA pair
-  const uint32_t lead_rank = rank & ~1u;                // the pair's leader (issues the MMAs)
-  const int half = LN ? static_cast<int>(rank >> 1) : 0;  // LN: which BN-column half of the rows
+  const uint32_t lead_rank = PAIR ? (rank & ~1u) : rank;  // the pair's leader (issues the MMAs)
+  const int half = LN ? static_cast<int>(DUO ? rank : rank >> 1) : 0;  // LN: which BN-column half of the rows
+  const uint32_t ln_partner = DUO ? (rank ^ 1u) : (rank ^ 2u);  // LN: the CTA holding the other half
   const bool leader = prank == 0;
-  const int unit0 = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
-  const int unit_step = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
+  const int unit0 = CLUSTER ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int unit_step = CLUSTER ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
   const int nb_units = LN ? 1 : n_blocks;
   const int num_units = ((m_blocks + (PAIR ? 1 : 0)) / (PAIR ? 2 : 1)) * nb_units;
   auto unit_m0 = [&](int u) { return ((u / nb_units) * (PAIR ? 2 : 1) + static_cast<int>(prank)) * BM; };
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       tmem_alloc<S::kTmemCols>(tmem_ptr);
   }
   tc_fence_before();
-  if (PAIR)
+  if (CLUSTER)
     cluster_sync_all();  // barrier inits visible cluster-wide before any remote complete_tx / arrive
   else
     __syncthreads();
@@ -233,6 +246,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     }
   }
   if (!late_wait) pdl_wait();  // the previous kernel's outputs (our A / residual) are complete and visible
+  if (!late_wait) KSPAN_WAITED(gemm, kSpanSlot);
   if (threadIdx.x == 0) GTRACE(2);
   pdl_trigger();
 
@@ -334,7 +348,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     float2* part = reinterpret_cast<float2*>(smem + S::kOffPart);  // [acc][hf][row]
     float2* recv = reinterpret_cast<float2*>(smem + S::kOffRecv);  // [acc][row]
     const uint32_t tmem_empty_lead0 = mapa_shared(&tmem_empty[0], lead_rank);
-    const uint32_t partner = rank ^ 2u;
+    const uint32_t partner = ln_partner;
     const uint32_t recv_remote0 = mapa_shared(recv, partner);
     const uint32_t xch_remote0 = mapa_shared(&xch_bar[0], partner);
     const int n_half0 = half * BN;
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     float2* part = reinterpret_cast<float2*>(smem + S::kOffPart);  // [acc][hf][row]
     float2* recv = reinterpret_cast<float2*>(smem + S::kOffRecv);  // [acc][row]
     const uint32_t tmem_empty_lead0 = mapa_shared(&tmem_empty[0], lead_rank);
-    const uint32_t partner = rank ^ 2u;
+    const uint32_t partner = ln_partner;
     const uint32_t recv_remote0 = mapa_shared(recv, partner);
     const uint32_t xch_remote0 = mapa_shared(&xch_bar[0], partner);
     const int n_half0 = half * BN;
@@ -697,9 +711,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
   }
 
   if (late_wait) pdl_wait();
+  if (late_wait) KSPAN_WAITED(gemm, kSpanSlot);
   if (threadIdx.x == 64) GTRACE(9);
   tc_fence_before();
-  if (PAIR)
+  if (CLUSTER)
     cluster_sync_all();  // the peers may still complete_tx / arrive on this CTA's barriers until here
   else
     __syncthreads();
@@ -710,6 +725,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     else
       tmem_dealloc<S::kTmemCols>(tmem_base);
   }
+  KSPAN_EXIT(gemm, kSpanSlot);
 }
 
 template <int BN, int STAGES, bool RESIDUAL, int CL, bool LN = false, bool LNREG = false, int ACT = CORA_ACT_NONE>
@@ -717,9 +733,10 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   constexpr int EW = epi_warps<LN, LNREG>();
   constexpr int kThreads = 64 + 32 * EW;
   using S = GemmSmem<BN, STAGES, CL, LN, (RESIDUAL && !LNREG) ? BN * 4 / EW / BK : (LNREG ? 0 : 1), EW>;
+  constexpr bool PAIR = CL == 4 || (CL == 2 && !LN);  // cta_group::2 (else single CTAs, DUO included)
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_2d_bf16(&ta, g.a, g.k, g.m, static_cast<uint64_t>(g.k) * 2, BK, BM, true) ||
-      !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, CL > 1 ? BN / 2 : BN, true) ||
+      !make_tmap_2d_bf16(&tb, g.b, g.k, g.n, static_cast<uint64_t>(g.k) * 2, BK, PAIR ? BN / 2 : BN, true) ||
       !make_tmap_2d_bf16(&tc, g.c, g.n, g.m, static_cast<uint64_t>(g.n) * 2, BK, kEpiRows, true))
     return cudaErrorInvalidValue;
   if (RESIDUAL) {
@@ -737,7 +754,7 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
     attr_set[dev] = true;
   }
   const int m_blocks = (g.m + BM - 1) / BM, n_blocks = (g.n + BN - 1) / BN;
-  const int units = ((m_blocks + (CL > 1 ? 1 : 0)) / (CL > 1 ? 2 : 1)) * (LN ? 1 : n_blocks);
+  const int units = ((m_blocks + (PAIR ? 1 : 0)) / (PAIR ? 2 : 1)) * (LN ? 1 : n_blocks);
   // persistent grid = the clusters that can be co-resident (clusters of 4 cannot use every SM: GPC
   // boundaries strand some), so no cluster waits for a second wave
   static int max_clusters_dev[kMaxDevices] = {};
@@ -800,6 +817,9 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   }
 }
 
+// 128-row units from which the short-K LN GEMM runs as DUOs (74 two-CTA clusters)
+constexpr int kLnDuoMinBlocks = 128;
+
 bool gemm_ln_supported(const GemmArgs& g) {
   // act NONE only (the layer's a4 / a7): with the activation variants compiled in, the fully unrolled
   // epilogue is 4x the code and a one-unit-per-CTA launch stalls on cold instruction fetches
@@ -813,7 +833,17 @@ cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream) {
   // 2 CTA pairs per cluster.  Long K (FF2): row segments in registers, one staging buffer, 5 stages --
   // the mainloop is bound by the bytes in flight.  Short K (out-proj): the epilogue is the critical path,
   // so the residual is TMA-prefetched into two staging buffers per warp (4 stages fit beside them).
+  // Long K (FF2) stays on 2 CTA pairs: a DUO CTA fills 48 KB of smem per k-block instead of 32 and its
+  // mainloop, bound by the bytes in flight, runs slower than the 16 SMs it gains (C4 FF2 + LN2 80 -> 83 us).
+  // Short K (out-proj, epilogue-bound) runs as DUOs once there are enough 128-row units to fill the
+  // 148 SMs in several waves (C4 out-proj + LN1 41.5 -> 36.9 us; at T ~ 1.5-6k the 4-CTA clusters are
+  // 0.2-0.5 us faster).  Both give bitwise the same output (test_ln_gemm_duo_bitwise).
+  // CORA_LN_DUO=0 / 1 forces the short-K choice (A/B runs).
+  static const int duo_env = getenv("CORA_LN_DUO") != nullptr ? atoi(getenv("CORA_LN_DUO")) : -1;
+  const int m_blocks = (g.m + BM - 1) / BM;
+  const bool duo = duo_env >= 0 ? duo_env != 0 : m_blocks >= kLnDuoMinBlocks;
   if (g.k >= 1024) return run_gemm<256, 6, true, 4, true, true>(g, stream);
+  if (duo) return run_gemm<256, 3, true, 2, true, false>(g, stream);
   return run_gemm<256, 4, true, 4, true, false>(g, stream);
 }
 

@@ -15,6 +15,8 @@
 #include "cora_internal.h"
 #include "ptx.cuh"
 
+CORA_KSPAN_DEFINE(prelude)
+
 namespace cora {
 
 namespace {
@@ -317,7 +319,9 @@ __global__ void __launch_bounds__(kScanThreads) layout_merged_kernel(
     int32_t* __restrict__ tile_seq, int32_t* __restrict__ n_tiles, int32_t* __restrict__ units,
     int32_t* __restrict__ unit_seq, int32_t* __restrict__ n_units, int32_t* __restrict__ status,
     int32_t* __restrict__ seq_of_tok, int32_t* __restrict__ pos_in_seq) {
+  KSPAN_ENTRY(prelude, 0);
   pdl_wait();  // the lengths may come from the previous kernel
+  KSPAN_WAITED(prelude, 0);
   pdl_trigger();
   extern __shared__ int32_t s_off[];  // [batch + 1] exclusive prefix of the (clamped) lengths
   const int32_t st = layout_scan_block(lengths, batch, total_tokens, heads, max_len, row_off, attn_off, tiles,
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(kScanThreads) layout_merged_kernel(
       pos_in_seq[o + i] = i;
     }
   }
+  KSPAN_EXIT(prelude, 0);
 }
 
 // f_fo / f_fi: for token t, b = max{b : row_off[b] <= t} (skips empty sequences), i = t - row_off[b].

@@ -198,7 +198,8 @@ def test_linear_epilogues(act, use_res, m, n, k):
     assert rel_err(to_np(c), ref) <= TOL_BF16
 
 
-@pytest.mark.parametrize("m,k", [(300, 512), (4099, 512), (257, 2048), (1000, 2048)])
+# (16500, 512): 129 row blocks, the short-K LN GEMM's DUO launch (csrc/gemm.cu launch_gemm_ln)
+@pytest.mark.parametrize("m,k", [(300, 512), (4099, 512), (16500, 512), (257, 2048), (1000, 2048)])
 @pytest.mark.parametrize("use_bias", [True, False])
 def test_linear_residual_layernorm_fused(m, k, use_bias):
     n = 512
@@ -238,6 +239,27 @@ def test_linear_residual_layernorm_large_mean_rows(k):
     big = np.abs(r.mean(1)) / r.std(1) >= 100
     assert big.sum() > m // 2
     assert rel_err(to_np(c), ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("k", [512, 2048])
+def test_ln_gemm_duo_bitwise(k):
+    """The rows of a GEMM + LayerNorm do not depend on the problem size: a 16 500-row problem (short K: DUO
+    launch, two single CTAs per 128 rows) and its first 4 099 and last 300 rows as problems of their own
+    (4-CTA clusters of CTA pairs) give bitwise the same rows, including rows with |mean| / sigma >= 100
+    (the statistics are merged in the same order by both launches)."""
+    m, n = 16500, 512
+    a = synth.round_bf16(synth.normal((m, k), 71))
+    w = synth.round_bf16(synth.normal((n, k), 72) / math.sqrt(k))
+    b = synth.round_bf16(synth.normal((n,), 73))
+    r = synth.round_bf16(synth.normal((m, n), 74))
+    r[::5] = synth.round_bf16(r[::5] * 0.01 + 2.0 ** 9)  # large-mean rows
+    g = synth.round_f32(1 + 0.1 * synth.normal((n,), 75))
+    be = synth.round_f32(0.1 * synth.normal((n,), 76))
+    A, W, B, R, G, BE = bf16_cuda(a), bf16_cuda(w), bf16_cuda(b), bf16_cuda(r), f32_cuda(g), f32_cuda(be)
+    big = P().linear_residual_layernorm(A, W, R, G, BE, bias=B)
+    for lo, hi in ((0, 4099), (m - 300, m)):
+        part = P().linear_residual_layernorm(A[lo:hi].contiguous(), W, R[lo:hi].contiguous(), G, BE, bias=B)
+        assert torch.equal(big[lo:hi], part), (lo, hi)
 
 
 def test_linear_residual_layernorm_unfused_no_activation():
