@@ -53,8 +53,21 @@ extern "C" int cora_debug_gemm_trace(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_gemm_trace, sizeof(unsigned long long) * (n < 2048 * 16 ? n : 2048 * 16)) ==
                  cudaSuccess ? 0 : 1;
 }
+// per-CTA wait totals (clock64 cycles) of the traced launch: [0] producer waiting for free stages, [1] MMA
+// waiting for loaded stages, [2] MMA waiting for a free accumulator, [3] MMA role total, [4] epilogue warp 0
+// waiting for its accumulator, [5] epilogue warp 0 total, [6] units of this CTA
+__device__ long long g_gemm_waits[2048][8];
+extern "C" int cora_debug_gemm_waits(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_gemm_waits, sizeof(g_gemm_waits)) == cudaSuccess ? 0 : 1;
+}
+#define GW_DECL long long gw_t0 = clock64(), gw_w = 0, gw_w2 = 0, gw_n = 0
+#define GW_WAIT(acc, stmt) do { const long long t_ = clock64(); stmt; acc += clock64() - t_; } while (0)
+#define GW_STORE(i, v) do { if (GTRACE_ON) g_gemm_waits[blockIdx.x][i] = (v); } while (0)
 #else
 #define GTRACE(k) ((void)0)
+#define GW_DECL
+#define GW_WAIT(acc, stmt) stmt
+#define GW_STORE(i, v) ((void)0)
 #endif
 
 CORA_KSPAN_DEFINE(gemm)
@@ -253,13 +266,14 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (every CTA)
     if (lane == 0) {
+      GW_DECL;
       int stage = 0;
       uint32_t phase = 0;
       for (int u = unit0; u < num_units; u += unit_step) {
         const int m0 = unit_m0(u), n0 = unit_n0(u);
         for (int kb = 0; kb < k_blocks; ++kb) {
           const bool b_issued = u == unit0 && kb < pre_b;  // fresh stage, B already in flight
-          if (!b_issued) mbar_wait(&empty[stage], phase ^ 1);
+          if (!b_issued) GW_WAIT(gw_w, mbar_wait(&empty[stage], phase ^ 1));
           uint8_t* sa = smem + S::kOffA + stage * S::kABytes;
           uint8_t* sb = smem + S::kOffB + stage * S::kBBytes;
           if (PAIR) {
@@ -276,6 +290,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
           if (++stage == STAGES) stage = 0, phase ^= 1;
         }
       }
+      GW_STORE(0, gw_w);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader, one thread)
@@ -285,12 +300,13 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      GW_DECL;
       for (int u = unit0; u < num_units; u += unit_step) {
-        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        GW_WAIT(gw_w2, mbar_wait(&tmem_empty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+          GW_WAIT(gw_w, mbar_wait(&full[stage], phase));
           if (u == unit0 && kb == 0) GTRACE(3);
           if (u == unit0 && kb == k_blocks / 2) GTRACE(4);
           if (u == unit0 && kb == k_blocks - 1) GTRACE(5);
@@ -323,7 +339,16 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
         else
           umma_commit(&tmem_full[acc]);
         if (++acc == 2) acc = 0, acc_phase ^= 1;
+#ifdef CORA_GEMM_TRACE
+        ++gw_n;
+#endif
       }
+      GW_STORE(1, gw_w);
+      GW_STORE(2, gw_w2);
+#ifdef CORA_GEMM_TRACE
+      GW_STORE(3, clock64() - gw_t0);
+      GW_STORE(6, gw_n);
+#endif
     }
   } else if (LN && LNREG) {
     // ------------------------------------------------------------ LN epilogue (every CTA)
@@ -610,6 +635,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     __nv_bfloat16* sbias = reinterpret_cast<__nv_bfloat16*>(smem + S::kOffBias + ew * S::kWarpCols * 2);
     uint64_t* rbar = res_bar + ew * S::kBufs;
     const uint32_t tmem_empty_lead0 = PAIR ? mapa_shared(&tmem_empty[0], lead_rank) : 0u;
+    GW_DECL;
     int acc = 0;
     uint32_t acc_phase = 0, res_phase = 0;
     for (int u = unit0; u < num_units; u += unit_step) {
@@ -634,7 +660,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
         *reinterpret_cast<uint4*>(sbias + g * 8) = bw;
       }
       __syncwarp();
+#ifdef CORA_GEMM_TRACE
+      GW_WAIT(gw_w, mbar_wait(&tmem_full[acc], acc_phase));
+#else
       mbar_wait(&tmem_full[acc], acc_phase);
+#endif
       if (u == unit0 && ew == 0 && lane == 0) GTRACE(6);
       tc_fence_after();
 #pragma unroll 1
@@ -708,6 +738,12 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     }
     if (lane == 0) tma_store_wait_all<0>();
     __syncwarp();
+#ifdef CORA_GEMM_TRACE
+    if (ew == 0 && lane == 0) {
+      GW_STORE(4, gw_w);
+      GW_STORE(5, clock64() - gw_t0);
+    }
+#endif
   }
 
   if (late_wait) pdl_wait();
