@@ -96,7 +96,10 @@ typedef struct cora_layout {
   int32_t* pos_in_seq;    /* [T]   f_fi: fused token index -> position i (f_oif(b,i) = row_off[b]+i) */
   int32_t* tiles;         /* [n_tiles_max] attention work list, longest first */
   int32_t* tile_seq;      /* [2*n_tiles_max] (row_off[b], L_b) of each work tile (one 8-byte load) */
-  int32_t* n_tiles;       /* [1]   number of valid entries of `tiles` (0 if status != 0) */
+  int32_t* n_tiles;       /* [3]   n_tiles[0]: number of valid entries of `tiles` (0 if status != 0);
+                             [1], [2]: the attention kernel's dynamic schedule (ticket counter, finished
+                             CTAs), zeroed by cora_layout_build and reset by every attention launch --
+                             attention launches on one layout must therefore not run concurrently */
   int32_t* status;        /* [1]   CORA_STATUS_* bits, 0 = ok */
   /* Attention work UNITS: pairs of consecutive q-tiles (2 qp, 2 qp + 1) of one (b, h) that share
    * their K/V tiles; same longest-first order.  Word layout as `tiles` with qt replaced by qp. */
@@ -104,7 +107,8 @@ typedef struct cora_layout {
   int32_t _pad2;
   int32_t* units;         /* [n_units_max] */
   int32_t* unit_seq;      /* [2*n_units_max] (row_off[b], L_b) of each unit */
-  int32_t* n_units;       /* [1]   number of valid entries of `units` (0 if status != 0) */
+  int32_t* n_units;       /* [3]   n_units[0]: number of valid entries of `units` (0 if status != 0);
+                             [1], [2]: the causal attention kernel's schedule words (as n_tiles) */
 } cora_layout_t;
 
 /* Encoder layer parameters (nn.Linear convention W[out, in], bf16; LayerNorm fp32).

@@ -51,6 +51,10 @@ constexpr int TK = 128;       // keys per KV tile
 constexpr int QSTAGES = 2;    // Q double buffer: the next tile's Q streams in under the current tile
 constexpr int KSTAGES = 3;    // K ring depth
 constexpr int VSTAGES = 2;    // V ring depth
+// Work schedule ring: entries published by the producer thread, read in order by the V producer, the MMA
+// thread (S and PV walks) and the 4 softmax warps -- 7 readers release each entry
+constexpr int kRing = 8;
+constexpr int kRingReaders = 7;
 // Warp roles.  Bidirectional kernel (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
 // warps 2-5 softmax.  Causal kernel (256 threads): warps 0 / 1 the same, warps 2-3 idle (they complete
 // warpgroup 0, whose registers go to the softmax warpgroup), warps 4-7 softmax.  Warp w of the softmax
@@ -122,10 +126,11 @@ struct AttnSmem {
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + QSTAGES * kTileBytes;
   static constexpr int kOffV = kOffK + KSTAGES * kTileBytes;
-  static constexpr int kOffMeta = kOffV + VSTAGES * kTileBytes;  // int4 [4 softmax warps][2 slots]
-  static constexpr int kOffBar = kOffMeta + 4 * 2 * 16;
-  // q_full/empty[QS], k_full/empty[KS], v_full/empty[VS], s_full, s_empty, p_full, pv_done, o_empty
-  static constexpr int kNumBars = 2 * (QSTAGES + KSTAGES + VSTAGES) + 5;
+  static constexpr int kOffRing = kOffV + VSTAGES * kTileBytes;  // int4 [kRing] the CTA's work schedule
+  static constexpr int kOffBar = kOffRing + kRing * 16;
+  // q_full/empty[QS], k_full/empty[KS], v_full/empty[VS], s_full, s_empty, p_full, pv_done, o_empty,
+  // ring_full/empty[kRing]
+  static constexpr int kNumBars = 2 * (QSTAGES + KSTAGES + VSTAGES) + 5 + 2 * kRing;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes;
 };
@@ -140,30 +145,51 @@ struct WorkTile {
   int h, qt, r0, L;
   bool packed;
 };
-// Metadata of work tile idx (two independent loads: the tile word and (row_off[b], L_b)).
-__device__ __forceinline__ WorkTile load_tile(const int32_t* tiles, const int2* tile_seq, int idx) {
-  const int32_t w = __ldg(tiles + idx);
-  const int2 sq = __ldg(tile_seq + idx);
-  return WorkTile{(w >> 16) & 0xFF, (w >> 24) & 0x7F, sq.x, sq.y, w < 0};
-}
-
 // The walk of one CTA: bidirectional attention visits single q-tiles of the longest-first tile list;
 // causal attention visits the UNIT list (same longest-first order, ceil(nq/2) units per (b, h)) and
 // processes unit qp as the q-tile pair (nq-1-qp, qp), whose KV work (nq-qp) + (qp+1) = nq+1 is the
-// same for every unit of a sequence (a lone middle tile when nq is odd), so the static stride over a
-// work-sorted list stays balanced although causal q-tiles have 1..nq KV tiles.
+// same for every unit of a sequence (a lone middle tile when nq is odd).  The entries are handed out
+// dynamically: CTA c starts with entry c, then each CTA's producer thread claims the next unclaimed
+// entry from a global ticket counter when it starts a tile (longest-processing-time-first: the list is
+// sorted by work, so the last entries handed out are the shortest), and publishes it to the CTA's roles
+// through the schedule ring.
 struct WorkUnit {
   int h, r0, L, qt0, qt1, count;
   bool packed;
   __device__ __forceinline__ WorkTile tile(int sub) const { return WorkTile{h, sub ? qt1 : qt0, r0, L, packed}; }
 };
+// A schedule entry: (idx, tile word, row_off[b], L_b) of a work-list entry, idx < 0 = end of the CTA's walk.
+__device__ __forceinline__ int4 sched_entry(const int32_t* list, const int2* list_seq, int idx, int n) {
+  if (idx >= n) return make_int4(-1, 0, 0, 0);
+  const int32_t w = __ldg(list + idx);
+  const int2 sq = __ldg(list_seq + idx);
+  return make_int4(idx, w, sq.x, sq.y);
+}
 template <bool CAUSAL>
-__device__ __forceinline__ WorkUnit load_work(const int32_t* list, const int2* list_seq, int idx) {
-  const WorkTile t = load_tile(list, list_seq, idx);
+__device__ __forceinline__ WorkUnit decode_work(int4 e) {
+  const WorkTile t{(e.y >> 16) & 0xFF, (e.y >> 24) & 0x7F, e.z, e.w, e.y < 0};
   if (!CAUSAL) return WorkUnit{t.h, t.r0, t.L, t.qt, t.qt, 1, t.packed};
   const int nq = (t.L + TQ - 1) / TQ, qp = t.qt;
   return WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2, t.packed};
 }
+// Reader of the schedule ring: entry k of the CTA's walk sits in slot k % kRing.  All lanes of a warp (or a
+// single thread) wait for the slot, read it and release it with one arrive.
+struct RingReader {
+  uint32_t ring;  // shared address of the int4 entries
+  uint64_t* full;
+  uint64_t* empty;
+  int k;
+  __device__ __forceinline__ int4 next(bool warp_wide) {
+    const int slot = k & (kRing - 1);
+    mbar_wait<false>(&full[slot], (k / kRing) & 1);
+    uint32_t a, b, c, d;
+    ld_shared_v4(ring + slot * 16, a, b, c, d);
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane_id() == 0) mbar_arrive(&empty[slot]);
+    ++k;
+    return make_int4(static_cast<int>(a), static_cast<int>(b), static_cast<int>(c), static_cast<int>(d));
+  }
+};
 
 // CAUSAL: masked MHA (App. D.3): query i attends to keys j <= i of its sequence, so
 // q-tile qt needs only KV tiles j <= qt (the "lower triangular" ragged loop -- tiles above the diagonal
@@ -171,7 +197,7 @@ __device__ __forceinline__ WorkUnit load_work(const int32_t* list, const int2* l
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ tiles,
-                         const int2* __restrict__ tile_seq, const int32_t* __restrict__ n_tiles_ptr,
+                         const int2* __restrict__ tile_seq, int32_t* __restrict__ n_tiles_ptr,
                          const int32_t* __restrict__ seq_of_tok, const int32_t* __restrict__ pos_in_seq,
                          const int32_t* __restrict__ lengths, __nv_bfloat16* __restrict__ out, int32_t d_model,
                          float scale_log2) {
@@ -192,6 +218,9 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
   uint64_t* p_full = s_empty + 1;
   uint64_t* pv_done = p_full + 1;
   uint64_t* o_empty = pv_done + 1;
+  uint64_t* ring_full = o_empty + 1;
+  uint64_t* ring_empty = ring_full + kRing;
+  const uint32_t ring_addr = smem_u32(smem + AttnSmem::kOffRing);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + AttnSmem::kNumBars);
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -215,45 +244,54 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     mbar_init(p_full, 4);
     mbar_init(pv_done, 1);
     mbar_init(o_empty, 4);
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&ring_full[r], 1);
+      mbar_init(&ring_empty[r], kRingReaders);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_ptr);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  // tmem_base / n_tiles / the first work unit: read before the role split (bidirectional), or by each role
-  // after its register reallocation (causal: values live across setmaxnreg are spilled)
+  // tmem_base: read before the role split (bidirectional), or by each role after its register reallocation
+  // (causal: values live across setmaxnreg are spilled)
   uint32_t tmem_base = 0;
-  int n_tiles = 0;
-  WorkUnit wu_next{};
   if constexpr (!CAUSAL) tmem_base = *tmem_ptr;
   pdl_wait();  // QKV (previous kernel) complete and visible
   KSPAN_WAITED(attn, 1);
   pdl_trigger();
-  if constexpr (!CAUSAL) {
-    n_tiles = *n_tiles_ptr;
-    // every role walks the same tiles; the next tile's metadata load is issued one tile ahead
-    if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
-  }
 
   if (warp < kSoftmaxWarp0<CAUSAL>) {
     // causal: warpgroup 0 (producer, MMA issuer, two idle warps) hands its registers to the softmax warpgroup
     if constexpr (CAUSAL) {
       setmaxnreg_dec<kRegsOther>();
       tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
-      n_tiles = *n_tiles_ptr;
-      if (static_cast<int>(blockIdx.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, blockIdx.x);
     }
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producers
     // lane 0 streams Q and K, lane 1 streams V: the two rings are refilled independently, so a V slot
     // still held by a pending PV never delays the next K load (and vice versa)
     if (lane == 0) {
+      // the scheduler: publishes entry k of the walk to ring slot k % kRing once all readers released it
+      const int n_tiles = *n_tiles_ptr;
+      int n_pub = 0;
+      auto publish = [&](int4 e) {
+        const int slot = n_pub & (kRing - 1);
+        if (n_pub >= kRing) mbar_wait<false>(&ring_empty[slot], ((n_pub / kRing) - 1) & 1);
+        st_shared_v4(ring_addr + slot * 16, static_cast<uint32_t>(e.x), static_cast<uint32_t>(e.y),
+                     static_cast<uint32_t>(e.z), static_cast<uint32_t>(e.w));
+        mbar_arrive(&ring_full[slot]);  // release: the entry is visible to the readers that see the phase
+        ++n_pub;
+      };
       uint32_t q_ph = 0, k_ph = 0;
       int qs = 0, ks = 0;
-      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkUnit wu = wu_next;
-        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+      int4 e = sched_entry(tiles, tile_seq, blockIdx.x, n_tiles);
+      publish(e);
+      // the next entry is claimed when a tile starts; its ticket is read after the tile's loads are issued
+      int ticket = e.x >= 0 ? atomicAdd(n_tiles_ptr + 1, 1) : 0;
+      while (e.x >= 0) {
+        const WorkUnit wu = decode_work<CAUSAL>(e);
         for (int sub = 0; sub < wu.count; ++sub) {
           const WorkTile cur = wu.tile(sub);
           const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
@@ -269,13 +307,16 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             if (++ks == KSTAGES) ks = 0, k_ph ^= 1;
           }
         }
+        e = sched_entry(tiles, tile_seq, static_cast<int>(gridDim.x) + ticket, n_tiles);
+        publish(e);
+        if (e.x >= 0) ticket = atomicAdd(n_tiles_ptr + 1, 1);
       }
     } else if (lane == 1) {
       uint32_t v_ph = 0;
       int vs = 0;
-      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkUnit wu = wu_next;
-        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+      RingReader rr{ring_addr, ring_full, ring_empty, 0};
+      for (int4 e = rr.next(false); e.x >= 0; e = rr.next(false)) {
+        const WorkUnit wu = decode_work<CAUSAL>(e);
         for (int sub = 0; sub < wu.count; ++sub) {
           const WorkTile cur = wu.tile(sub);
           const int nkv = CAUSAL ? min((cur.L + TK - 1) / TK, cur.qt + 1) : (cur.L + TK - 1) / TK;
@@ -302,20 +343,21 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
       // The S iterator walks the flattened (tile, KV step) sequence one step ahead of the PV loop, across
       // tile boundaries: the next tile's S_0 is issued before this tile's last PV, so the softmax warps find
       // it ready when they finish the tile (their epilogue of the tile is deferred into the next one).
-      int s_idx = blockIdx.x, s_sub = 0, s_j = 0, s_nkv = 0, s_qs = 0;
+      int s_sub = 0, s_j = 0, s_nkv = 0, s_qs = 0;
       uint32_t s_qph = 0;
-      WorkUnit s_wu{}, s_wu_next{};
       auto tile_nkv = [](const WorkTile& t) {
         return CAUSAL ? min((t.L + TK - 1) / TK, t.qt + 1) : (t.L + TK - 1) / TK;
       };
-      if (s_idx < n_tiles) {
-        s_wu = wu_next;
+      // two walks of the schedule: the S iterator (one KV step ahead) and the PV loop
+      RingReader rs{ring_addr, ring_full, ring_empty, 0}, rp{ring_addr, ring_full, ring_empty, 0};
+      int4 s_e = rs.next(false);
+      WorkUnit s_wu{};
+      if (s_e.x >= 0) {
+        s_wu = decode_work<CAUSAL>(s_e);
         s_nkv = tile_nkv(s_wu.tile(0));
-        if (s_idx + static_cast<int>(gridDim.x) < n_tiles)
-          s_wu_next = load_work<CAUSAL>(tiles, tile_seq, s_idx + gridDim.x);
       }
       auto issue_next_s = [&]() {
-        if (s_idx >= n_tiles) return;
+        if (s_e.x < 0) return;
         ATR_MMA(20);
         if (s_j == 0) mbar_wait<false>(&q_full[s_qs], s_qph);
         mbar_wait<false>(&k_full[ks], k_ph);
@@ -339,18 +381,15 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           s_j = 0;
           if (++s_sub == s_wu.count) {
             s_sub = 0;
-            s_idx += gridDim.x;
-            s_wu = s_wu_next;
-            if (s_idx + static_cast<int>(gridDim.x) < n_tiles)
-              s_wu_next = load_work<CAUSAL>(tiles, tile_seq, s_idx + gridDim.x);
+            s_e = rs.next(false);
+            if (s_e.x >= 0) s_wu = decode_work<CAUSAL>(s_e);
           }
-          if (s_idx < n_tiles) s_nkv = tile_nkv(s_wu.tile(s_sub));
+          if (s_e.x >= 0) s_nkv = tile_nkv(s_wu.tile(s_sub));
         }
       };
       issue_next_s();
-      for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x) {
-        const WorkUnit wu = wu_next;
-        if (idx + static_cast<int>(gridDim.x) < n_tiles) wu_next = load_work<CAUSAL>(tiles, tile_seq, idx + gridDim.x);
+      for (int4 e = rp.next(false); e.x >= 0; e = rp.next(false)) {
+        const WorkUnit wu = decode_work<CAUSAL>(e);
         for (int sub = 0; sub < wu.count; ++sub) {
           const int nkv = tile_nkv(wu.tile(sub));
           for (int j = 0; j < nkv; ++j) {
@@ -387,7 +426,6 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     if constexpr (CAUSAL) {
       setmaxnreg_inc<kRegsSoftmax>();
       tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
-      n_tiles = *n_tiles_ptr;
     }
     const uint32_t qd = warp & 3;  // TMEM lane quadrant
     const bool out_v8 = (reinterpret_cast<uintptr_t>(out) & 31u) == 0 && (d_model % 16) == 0 && (HD % 16) == 0;
@@ -397,36 +435,14 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
 #ifdef CORA_ATTN_TRACE
     int atr_n = 0;
 #endif
-    // the next tile's metadata is prefetched one tile ahead into shared memory with cp.async (no
-    // registers held while in flight; prefetching into registers spilled)
-    int4* meta = reinterpret_cast<int4*>(smem + AttnSmem::kOffMeta) + qd * 2;  // [2 slots] per warp
-    auto prefetch_meta = [&](int idx, int slot) {
-      if (lane == 0 && idx < n_tiles) {
-        cp_async_4(&meta[slot].x, tiles + idx);
-        cp_async_8(&meta[slot].z, tile_seq + idx);
-      }
-      cp_async_commit();
-    };
-    int slot = 0;
-    prefetch_meta(blockIdx.x, 0);
-    for (int idx = blockIdx.x; idx < n_tiles; idx += gridDim.x, slot ^= 1) {
+    // the walk's entries come from the schedule ring (published by the producer thread a tile ahead)
+    RingReader rw{ring_addr, ring_full, ring_empty, 0};
+    while (true) {
       ATR_SM(11);
-      cp_async_wait_all();
+      const int4 mt = rw.next(true);
       ATR_SM(12);
-      __syncwarp();
-      const int4 mt = meta[slot];
-      __syncwarp();
-      prefetch_meta(idx + gridDim.x, slot ^ 1);
-      WorkUnit wu;
-      {
-        const WorkTile t{(mt.x >> 16) & 0xFF, (mt.x >> 24) & 0x7F, mt.z, mt.w, mt.x < 0};
-        if (!CAUSAL) {
-          wu = WorkUnit{t.h, t.r0, t.L, t.qt, t.qt, 1, t.packed};
-        } else {
-          const int nq = (t.L + TQ - 1) / TQ, qp = t.qt;
-          wu = WorkUnit{t.h, t.r0, t.L, nq - 1 - qp, qp, (nq - 1 - qp == qp) ? 1 : 2, t.packed};
-        }
-      }
+      if (mt.x < 0) break;
+      const WorkUnit wu = decode_work<CAUSAL>(mt);
       for (int sub = 0; sub < wu.count; ++sub) {
         const WorkTile cur = wu.tile(sub);
         const int L = cur.L;
@@ -679,6 +695,15 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  // the last CTA to finish resets the ticket counter for the next launch on this layout (every CTA has
+  // claimed its last entry before it gets here; the next launch reads the counter after griddepcontrol.wait)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(n_tiles_ptr + 2, 1) == static_cast<int>(gridDim.x) - 1) {
+      atomicExch(n_tiles_ptr + 1, 0);
+      atomicExch(n_tiles_ptr + 2, 0);
+    }
+  }
   KSPAN_EXIT(attn, 1);
 }
 

@@ -9,9 +9,10 @@
 #include "../../include/cora.h"
 
 // Kernel spans (profiling builds only, -DCORA_KSPAN): per kernel slot, %globaltimer of the first CTA entry,
-// the last CTA exit and the first / last return from griddepcontrol.wait, collected with 64-bit atomics.
+// the last CTA exit and the first / last return from griddepcontrol.wait, the sum (low 40 bits) and count of the CTA
+// exits (mean exit: the kernel's tail), collected with 64-bit atomics.
 // Slots: 0 prelude, 1 attention, 2 QKV, 3 out-proj + LN1, 4 FF1, 5 FF2 + LN2.  Each translation unit owns
-// its array (no relocatable device code) and exports cora_debug_kspan_<tu>(host[8][4], reset).
+// its array (no relocatable device code) and exports cora_debug_kspan_<tu>(host[8][6], reset).
 #ifdef CORA_KSPAN
 __device__ __forceinline__ unsigned long long kspan_now() {
   unsigned long long t;
@@ -19,17 +20,26 @@ __device__ __forceinline__ unsigned long long kspan_now() {
   return t;
 }
 #define CORA_KSPAN_DEFINE(tu)                                                                            \
-  __device__ unsigned long long g_kspan_##tu[8][4];                                                      \
+  __device__ unsigned long long g_kspan_##tu[8][6];                                                      \
   extern "C" int cora_debug_kspan_##tu(unsigned long long* host, int reset) {                           \
     if (reset) {                                                                                         \
-      unsigned long long init[8][4];                                                                     \
-      for (int i = 0; i < 8; ++i) init[i][0] = init[i][3] = ~0ull, init[i][1] = init[i][2] = 0ull;      \
+      unsigned long long init[8][6];                                                                     \
+      for (int i = 0; i < 8; ++i)                                                                        \
+        init[i][0] = init[i][3] = ~0ull, init[i][1] = init[i][2] = init[i][4] = init[i][5] = 0ull;      \
       return cudaMemcpyToSymbol(g_kspan_##tu, init, sizeof(init)) == cudaSuccess ? 0 : 1;               \
     }                                                                                                    \
     return cudaMemcpyFromSymbol(host, g_kspan_##tu, sizeof(g_kspan_##tu)) == cudaSuccess ? 0 : 1;       \
   }
 #define KSPAN_ENTRY(tu, slot) do { if (threadIdx.x == 0) atomicMin(&g_kspan_##tu[slot][0], kspan_now()); } while (0)
-#define KSPAN_EXIT(tu, slot) do { if (threadIdx.x == 0) atomicMax(&g_kspan_##tu[slot][1], kspan_now()); } while (0)
+#define KSPAN_EXIT(tu, slot)                                                                             \
+  do {                                                                                                   \
+    if (threadIdx.x == 0) {                                                                              \
+      const unsigned long long t_ = kspan_now();                                                         \
+      atomicMax(&g_kspan_##tu[slot][1], t_);                                                             \
+      atomicAdd(&g_kspan_##tu[slot][4], t_ & ((1ull << 40) - 1));                                                        \
+      atomicAdd(&g_kspan_##tu[slot][5], 1ull);                                                           \
+    }                                                                                                    \
+  } while (0)
 #define KSPAN_WAITED(tu, slot)                                                                           \
   do {                                                                                                   \
     if (threadIdx.x == 0) {                                                                              \

@@ -218,6 +218,9 @@ __device__ __forceinline__ int32_t layout_scan_block(const int32_t* __restrict__
     // packed: the one-tile sequences' heads * hist[1] entries become heads * (windows) entries
     *n_tiles = st ? 0 : (pack ? bucket_base[1] + heads * s_nwin : s_tot);
     *n_units = st ? 0 : (pack ? unit_base[1] + heads * s_nwin : s_utot);
+    // the attention kernels' dynamic schedule words (ticket, finished CTAs) live after each count
+    n_tiles[1] = n_tiles[2] = 0;
+    n_units[1] = n_units[2] = 0;
   }
   if (st) return st;  // data error: empty work list, nothing else is read
   const int32_t* roff = s_off != nullptr ? s_off : row_off;  // this CTA's copy of the exclusive prefix

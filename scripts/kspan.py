@@ -2,7 +2,7 @@
     CORA_LIB_PATH=variants/kspan.so python scripts/kspan.py [config[,config...]] [reps]
 Configs: synth names (C4-wiki512, C2-mnli, ...), <dataset>-<batch> (mnli-32), or shard<N> (rank 0's shard
 of C4 at N ranks).  Per kernel (slot order = launch order): first CTA entry, first / last return from
-griddepcontrol.wait, last CTA exit, in us from the step's first entry; medians over reps, L2 flushed
+griddepcontrol.wait, last CTA exit, tail = last minus mean CTA exit, in us from the step's first entry; medians over reps, L2 flushed
 (256 MB write + read) before each replay as in bench.py.
 """
 import ctypes
@@ -42,7 +42,7 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 9
     lib = _lib.lib()
     tus = [getattr(lib, f"cora_debug_kspan_{t}") for t in ("prelude", "attn", "gemm")]
-    buf = (ctypes.c_ulonglong * 32)()
+    buf = (ctypes.c_ulonglong * 48)()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for cfg in cfgs:
         lengths, d, H, dff = lengths_of(cfg)
@@ -75,22 +75,26 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             steps.append(e0.elapsed_time(e1) * 1e3)
-            span = np.zeros((8, 4), dtype=np.float64)
+            span = np.zeros((8, 6), dtype=np.int64)
             for si, f in enumerate(tus):
                 f(buf, 0)
-                a = np.frombuffer(buf, dtype=np.uint64).reshape(8, 4).astype(np.float64)
+                a = np.frombuffer(buf, dtype=np.uint64).reshape(8, 6).astype(np.int64)
+                # mean exit from the low 40 bits of the exits (the device sums those): max exit - its tail
+                low = a[:, 1] & ((1 << 40) - 1)
+                a[:, 4] = np.where(a[:, 5] > 0, a[:, 1] - (low - a[:, 4] // np.maximum(a[:, 5], 1)), 0)
                 slots = [0] if si == 0 else ([1] if si == 1 else [2, 3, 4, 5])
                 for s in slots:
                     span[s] = a[s]
             t0 = min(span[s][0] for s in range(6))
-            rows.append((span[:6] - t0) / 1e3)
+            r = (span[:6, :5] - t0).astype(np.float64) / 1e3
+            rows.append(r)
         med = np.median(np.stack(rows), axis=0)
         print(f"== {cfg}: B={len(lengths)} T={T}  step (events) median {np.median(steps):.1f} us")
-        print(f"  {'kernel':<12} {'entry':>7} {'wait0':>7} {'wait1':>7} {'exit':>7} | {'wait1->exit':>11}")
+        print(f"  {'kernel':<12} {'entry':>7} {'wait0':>7} {'wait1':>7} {'exit':>7} | {'wait1->exit':>11} {'tail':>6}")
         prev_exit = 0.0
         for s in ORDER:
-            e, w1, w0, x_ = med[s][0], med[s][2], med[s][3], med[s][1]
-            print(f"  {NAMES[s]:<12} {e:7.1f} {w0:7.1f} {w1:7.1f} {x_:7.1f} | {x_ - w1:11.1f}")
+            e, w1, w0, x_, xm = med[s][0], med[s][2], med[s][3], med[s][1], med[s][4]
+            print(f"  {NAMES[s]:<12} {e:7.1f} {w0:7.1f} {w1:7.1f} {x_:7.1f} | {x_ - w1:11.1f} {x_ - xm:6.1f}")
         sys.stdout.flush()
 
 
