@@ -15,7 +15,14 @@ import synth
 
 
 def _config(name):
-    """synth.config names, or ds:<dataset>:<batch> (Table 3 length generator, d 512 / 8 heads / 2048)."""
+    """synth.config names, ds:<dataset>:<batch> (Table 3 length generator, d 512 / 8 heads / 2048), or
+    shard<N> (rank 0's shard of C4 at N ranks)."""
+    if name.startswith("shard"):
+        from paper_2110_10221_b200.dist import shard_rows
+        lengths, d, H, dff = synth.config("C4-wiki512")
+        lengths = np.asarray(lengths, np.int64)
+        plan, _ = shard_rows(list(lengths), d, dff, int(name[5:]))
+        return lengths[plan[0]:plan[1]], d, H, dff
     if name.startswith("ds:"):
         _, ds, bs = name.split(":")
         return synth.dataset_lengths(ds, int(bs)), 512, 8, 2048
