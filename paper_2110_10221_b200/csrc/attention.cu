@@ -54,18 +54,34 @@ constexpr int VSTAGES = 2;    // V ring depth
 // Work schedule ring: entries published by the producer thread, read in order by the V producer, the MMA
 // thread (S and PV walks) and the 4 softmax warps -- 7 readers release each entry
 constexpr int kRing = 8;
-constexpr int kRingReaders = 7;
 // Warp roles.  Bidirectional kernel (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
 // warps 2-5 softmax.  Causal kernel (256 threads): warps 0 / 1 the same, warps 2-3 idle (they complete
 // warpgroup 0, whose registers go to the softmax warpgroup), warps 4-7 softmax.  Warp w of the softmax
 // reads TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31.
+// Bidirectional kernel (384 threads): warpgroup 2 (warps 8-11) is the tile epilogue -- it waits for the
+// tile's last PV, reads O out of TMEM, normalises it by the row sums the softmax warps leave in shared memory
+// and stores it -- so the softmax warps go straight on to the next tile's S_0.
 template <bool CAUSAL>
-constexpr int kThreadsOf = CAUSAL ? 256 : 192;
+constexpr bool kEpiWG = !CAUSAL;
 template <bool CAUSAL>
-constexpr uint32_t kSoftmaxWarp0 = CAUSAL ? 4 : 2;
+constexpr int kThreadsOf = CAUSAL ? 256 : 384;
+template <bool CAUSAL>
+constexpr uint32_t kSoftmaxWarp0 = 4;
+constexpr uint32_t kEpiWarp0 = 8;
+// ring readers: V producer, two MMA walks, 4 softmax warps (+ 4 epilogue warps)
+template <bool CAUSAL>
+constexpr int kRingReadersOf = kEpiWG<CAUSAL> ? 11 : 7;
 // causal: 2 CTAs x 256 threads x 128 registers at launch; setmaxnreg: 128 x 56 + 128 x 200 = 256 x 128 (the
-// per-chunk liveness of the diagonal / tail tiles needs more than the 168 registers of 192 threads)
-constexpr uint32_t kRegsSoftmax = 200, kRegsOther = 56;
+// per-chunk liveness of the diagonal / tail tiles needs more than the 168 registers of 192 threads).
+// bidirectional: 2 CTAs x 384 threads x 80 registers; 128 x (40 + 160 + 40) = 384 x 80.
+#ifndef CORA_ATTN_REGS_SM
+#define CORA_ATTN_REGS_SM 160
+#endif
+template <bool CAUSAL>
+constexpr uint32_t kRegsSoftmax = CAUSAL ? 200 : CORA_ATTN_REGS_SM;
+template <bool CAUSAL>
+constexpr uint32_t kRegsOther = CAUSAL ? 56 : (240 - CORA_ATTN_REGS_SM) / 2;
+constexpr uint32_t kRegsEpi = (240 - CORA_ATTN_REGS_SM) / 2;
 constexpr int kTileBytes = TQ * HD * 2;  // 16 KB, also the K and V tile size
 // Lazy rescaling (reading a3-r1): the running reference max m_ref of a row is only
 // moved when a new score exceeds it by more than kRescaleLog2 (in log2 units), so P <= 2^8 and the
@@ -127,10 +143,11 @@ struct AttnSmem {
   static constexpr int kOffK = kOffQ + QSTAGES * kTileBytes;
   static constexpr int kOffV = kOffK + KSTAGES * kTileBytes;
   static constexpr int kOffRing = kOffV + VSTAGES * kTileBytes;  // int4 [kRing] the CTA's work schedule
-  static constexpr int kOffBar = kOffRing + kRing * 16;
+  static constexpr int kOffL = kOffRing + kRing * 16;            // float [TQ] row sums softmax -> epilogue
+  static constexpr int kOffBar = kOffL + TQ * 4;
   // q_full/empty[QS], k_full/empty[KS], v_full/empty[VS], s_full, s_empty, p_full, pv_done, o_empty,
-  // ring_full/empty[kRing]
-  static constexpr int kNumBars = 2 * (QSTAGES + KSTAGES + VSTAGES) + 5 + 2 * kRing;
+  // ring_full/empty[kRing], l_full, l_empty
+  static constexpr int kNumBars = 2 * (QSTAGES + KSTAGES + VSTAGES) + 5 + 2 * kRing + 2;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAlloc = kBytes;
 };
@@ -220,6 +237,9 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
   uint64_t* o_empty = pv_done + 1;
   uint64_t* ring_full = o_empty + 1;
   uint64_t* ring_empty = ring_full + kRing;
+  uint64_t* l_full = ring_empty + kRing;
+  uint64_t* l_empty = l_full + 1;
+  float* lbuf = reinterpret_cast<float*>(smem + AttnSmem::kOffL);
   const uint32_t ring_addr = smem_u32(smem + AttnSmem::kOffRing);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + AttnSmem::kNumBars);
 
@@ -246,28 +266,26 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
     mbar_init(o_empty, 4);
     for (int r = 0; r < kRing; ++r) {
       mbar_init(&ring_full[r], 1);
-      mbar_init(&ring_empty[r], kRingReaders);
+      mbar_init(&ring_empty[r], kRingReadersOf<CAUSAL>);
     }
+    mbar_init(l_full, 4);
+    mbar_init(l_empty, 4);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_ptr);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  // tmem_base: read before the role split (bidirectional), or by each role after its register reallocation
-  // (causal: values live across setmaxnreg are spilled)
+  // tmem_base: read by each role after its register reallocation (values live across setmaxnreg are spilled)
   uint32_t tmem_base = 0;
-  if constexpr (!CAUSAL) tmem_base = *tmem_ptr;
   pdl_wait();  // QKV (previous kernel) complete and visible
   KSPAN_WAITED(attn, 1);
   pdl_trigger();
 
   if (warp < kSoftmaxWarp0<CAUSAL>) {
-    // causal: warpgroup 0 (producer, MMA issuer, two idle warps) hands its registers to the softmax warpgroup
-    if constexpr (CAUSAL) {
-      setmaxnreg_dec<kRegsOther>();
-      tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
-    }
+    // warpgroup 0 (producer, MMA issuer, two idle warps) hands its registers to the softmax warpgroup
+    setmaxnreg_dec<kRegsOther<CAUSAL>>();
+    tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producers
     // lane 0 streams Q and K, lane 1 streams V: the two rings are refilled independently, so a V slot
@@ -421,12 +439,10 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
       ATR_DONE(1);
     }
   }
-  } else {
-    // ------------------------------------------------------------ softmax / correction / epilogue
-    if constexpr (CAUSAL) {
-      setmaxnreg_inc<kRegsSoftmax>();
-      tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
-    }
+  } else if (!kEpiWG<CAUSAL> || warp < kEpiWarp0) {
+    // ------------------------------------------------------------ softmax / correction (/ epilogue)
+    setmaxnreg_inc<kRegsSoftmax<CAUSAL>>();
+    tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
     const uint32_t qd = warp & 3;  // TMEM lane quadrant
     const bool out_v8 = (reinterpret_cast<uintptr_t>(out) & 31u) == 0 && (d_model % 16) == 0 && (HD % 16) == 0;
     const int i = qd * 32 + lane;  // query row within the tile
@@ -435,6 +451,17 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
 #ifdef CORA_ATTN_TRACE
     int atr_n = 0;
 #endif
+    // epilogue warpgroup: the previous tile's last PV has not been waited for (its P columns are reused by
+    // this tile's P_0); l_n: row sums handed over so far
+    bool pv_pending = false;
+    int l_n = 0;
+    auto hand_l = [&](float lv) {
+      if (l_n > 0) mbar_wait<false>(l_empty, (l_n - 1) & 1);  // the epilogue has read the previous tile's
+      lbuf[i] = lv;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(l_full);
+      ++l_n;
+    };
     // the walk's entries come from the schedule ring (published by the producer thread a tile ahead)
     RingReader rw{ring_addr, ring_full, ring_empty, 0};
     while (true) {
@@ -457,12 +484,18 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_empty);
-            if (j > 0) {
+            if (j > 0 || pv_pending) {
               mbar_wait<false>(pv_done, pv_ph);
               pv_ph ^= 1;
+              pv_pending = false;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
+          }
+          if constexpr (kEpiWG<CAUSAL>) {
+            hand_l(0.f);  // keeps the handshake; the epilogue stores nothing for this warp
+            pv_pending = true;
+            continue;
           }
           mbar_wait<false>(pv_done, pv_ph);
           pv_ph ^= 1;
@@ -619,10 +652,11 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           }
           ATR_SM(5);
           l = l * alpha + (((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7])));
-          if (j > 0) {  // PV_{j-1} has consumed P_{j-1} and accumulated into O
+          if (j > 0 || pv_pending) {  // PV_{j-1} (or the previous tile's last PV) has consumed its P
             mbar_wait<false>(pv_done, pv_ph);
             pv_ph ^= 1;
             tc_fence_after();
+            pv_pending = false;
           }
           ATR_SM(6);
           CORA_TMEM_ST_32X32B_X32(tmem_base + t_lane + kTmemP, pk);
@@ -645,6 +679,11 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
           ATR_SM(7);
+        }
+        if constexpr (kEpiWG<CAUSAL>) {  // the epilogue warpgroup normalises and stores O
+          hand_l(l);
+          pv_pending = true;
+          continue;
         }
         // epilogue: wait for the last PV, normalise, store the valid query rows of this tile
         mbar_wait<false>(pv_done, pv_ph);
@@ -690,6 +729,70 @@ __global__ void __launch_bounds__(kThreadsOf<CAUSAL>, 2)
       }
     }
     if (qd == 0 && lane == 0) ATR_DONE(0);
+  } else {
+    // ------------------------------------------------------------ tile epilogue (bidirectional kernel)
+    // Warp w reads TMEM lanes 32 (w % 4) ..: per tile, the row sum l of its row (shared memory, handed over
+    // after the softmax warps stored the tile's last P -- by then every PV but the last has completed, so the
+    // parity wait below is for that last PV), then O in four 16-column chunks; the O columns are released
+    // to the MMA thread (the next tile's first PV) after the last chunk is read.
+    if constexpr (kEpiWG<CAUSAL>) {
+      setmaxnreg_dec<kRegsEpi>();
+      tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_ptr);
+      const uint32_t qd = warp & 3;
+      const int i = qd * 32 + lane;
+      const uint32_t t_lane = (qd * 32) << 16;
+      const bool out_v8 = (reinterpret_cast<uintptr_t>(out) & 31u) == 0 && (d_model % 16) == 0;
+      int pv_n = 0, l_n = 0;
+      RingReader rw{ring_addr, ring_full, ring_empty, 0};
+      for (int4 mt = rw.next(true); mt.x >= 0; mt = rw.next(true)) {
+        const WorkUnit wu = decode_work<CAUSAL>(mt);
+        for (int sub = 0; sub < wu.count; ++sub) {
+          const WorkTile cur = wu.tile(sub);
+          const int L = cur.L;
+          pv_n += (L + TK - 1) / TK;
+          mbar_wait<false>(l_full, l_n & 1);
+          const float lv = lbuf[i];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(l_empty);
+          ++l_n;
+          mbar_wait<false>(pv_done, (pv_n - 1) & 1);
+          tc_fence_after();
+          const int qrow = cur.qt * TQ + i;
+          if (cur.qt * TQ + static_cast<int>(qd) * 32 < L) {
+            const float inv = qrow < L ? rcp_fma(lv) : 0.f;
+            __nv_bfloat16* orow = out + static_cast<size_t>(cur.r0 + qrow) * d_model + cur.h * HD;
+  #pragma unroll
+            for (int g = 0; g < HD / 16; ++g) {
+              uint32_t r[16];
+              CORA_TMEM_LD_32X32B_X16(tmem_base + t_lane + kTmemO + g * 16, r);
+              tmem_ld_wait();
+              if (g == HD / 16 - 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(o_empty);
+              }
+              if (qrow < L) {
+                uint32_t w[8];
+  #pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  w[e] = pack_bf16x2(__uint_as_float(r[2 * e]) * inv, __uint_as_float(r[2 * e + 1]) * inv);
+                if (out_v8) {
+                  st_global_v8(orow + g * 16, w);
+                } else {
+                  uint4* dst = reinterpret_cast<uint4*>(orow + g * 16);
+                  dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                  dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                }
+              }
+            }
+          } else {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(o_empty);
+          }
+        }
+      }
+    }
   }
 
   tc_fence_before();
