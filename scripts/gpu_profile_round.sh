@@ -7,8 +7,14 @@ mkdir -p "$OUT"
 : > "$OUT/summary.txt"
 timeout 600 python -m pytest tests/ -q -m gpu -x --timeout 180 -p no:cacheprovider > "$OUT/tests.log" 2>&1
 echo "tests exit $?" >> "$OUT/summary.txt"
-timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
+# the driver's command (20 timed steps after 5 warm-up) is the headline; 200 steps show the power-capped state
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"
 echo "bench exit $?" >> "$OUT/summary.txt"
+sleep 10
+timeout 900 python bench.py --steps 200 --warmup 10 --no-e2e --no-cpu --no-stack > "$OUT/bench200.json" 2> "$OUT/bench200.err"
+echo "bench200 exit $?" >> "$OUT/summary.txt"
+timeout 600 python scripts/step_modes.py C4-wiki512 300 > "$OUT/step_modes.txt" 2>&1
+echo "step_modes exit $?" >> "$OUT/summary.txt"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-clocks --no-stack --no-ex2 > "$OUT/ncu_bench.log" 2>&1
 echo "ncu launches exit $?" >> "$OUT/summary.txt"
