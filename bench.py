@@ -254,6 +254,8 @@ def main():
     ap.add_argument("--groups", type=int, default=4,
                     help="N > 1 6-layer stack: groups per rank whose gather overlaps the next group's compute")
     ap.add_argument("--no-clocks", action="store_true", help="do not run the nvidia-smi sampler (use under ncu)")
+    ap.add_argument("--prewarm", type=int, default=3,
+                    help="untimed graph replays (each after an L2 flush) enqueued just before the timed steps")
     ap.add_argument("--no-ex2", action="store_true", help="skip the EX2 peak microbenchmark (use under ncu)")
     ap.add_argument("--debug-gloo", action="store_true",
                     help="N > 1 control-flow check on ONE GPU: ranks share the device, gloo process group, the "
@@ -417,6 +419,13 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        # warm-up replays enqueued right before the timed steps (outside the events), so the timed region
+        # does not start on a GPU that idled while the clock sampler started
+        if graph is not None:
+            for _ in range(args.prewarm):
+                if not args.no_flush:
+                    flush_l2()
+                graph.replay()
         # ---- the timed region: exactly K steps
         if graph is not None:
             step_ms = timed(graph.replay, args.steps)
