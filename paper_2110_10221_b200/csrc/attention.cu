@@ -18,14 +18,18 @@
 //                                  pairs, V an MN-major smem operand; O in TMEM cols [192,256))
 //                the S MMAs run one KV step ahead of the PV MMAs over the CTA's whole work list, so the
 //                next tile's S_0 is issued before this tile's last PV
-//   warps 2..5 : softmax / correction / epilogue, one query row per thread (TMEM lane = row):
+//   warps 4..7 : softmax / correction, one query row per thread (TMEM lane = row):
 //                  S_j is read from TMEM in one pass and the buffer released at once (so S_{j+1}
 //                  overlaps the exponentials), online softmax in the exp2 domain with a lazily
 //                  moved reference max, masking keys >= L_b with -inf in the tail tile only
 //                  (reading c18), P_j -> bf16 pairs -> TMEM (tcgen05.st; A operand of the PV MMA);
 //                  O accumulates in TMEM across KV tiles (rescaled in place only when the
-//                  reference max moves); o / l -> bf16 -> predicated row stores (rows >= L_b
-//                  belong to the next sequence and are never written).
+//                  reference max moves); the row sums l go to shared memory for the epilogue.
+//   warps 8..11: (bidirectional kernel) tile epilogue: wait for the tile's last PV, read O out of TMEM,
+//                  o / l -> bf16 -> predicated row stores (rows >= L_b belong to the next sequence and are
+//                  never written), so the softmax warps start the next tile right after its last P.  The
+//                  causal kernel (256 threads; its softmax warps need 200 registers) keeps this epilogue in
+//                  the softmax warps.  warps 2..3 complete warpgroup 0 (setmaxnreg works per warpgroup).
 // Rows of a 128-row TMA box that lie past the sequence end are real rows of the next
 // sequence (finite) or TMA zero-fill past T: their keys are masked and their queries discarded.
 // Two CTAs per SM (112 KB smem, 256 TMEM columns each) overlap one CTA's softmax with the other's MMAs.
