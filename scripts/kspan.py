@@ -49,7 +49,13 @@ def main():
         lengths = [int(v) for v in lengths]
         T = sum(lengths)
         params = P.EncoderParams.from_host(synth.encoder_weights(d, H, dff))
-        fwd = P.EncoderForward(params)
+        if os.environ.get("KSPAN_SPLIT"):  # prelude, then the layer (the QKV GEMM waits for the prelude)
+            layer = P.EncoderLayer(params)
+
+            def fwd(Lt, T, x, out):
+                layer(x, P.layout_build(Lt, T, H, 512), out=out)
+        else:
+            fwd = P.EncoderForward(params)
         Lt = torch.tensor(lengths, dtype=torch.int32, device="cuda")
         x = torch.randn(T, d, device="cuda").to(torch.bfloat16)
         y = torch.empty_like(x)
