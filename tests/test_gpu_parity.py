@@ -608,6 +608,22 @@ def test_layer_events_and_user_stream():
     assert all(ev[i].elapsed_time(ev[i + 1]) >= 0 for i in range(7))
 
 
+def test_layer_run_to_run_bitwise():
+    """The attention kernel hands out its work list dynamically (which CTA runs which tile changes from run to
+    run) and hands each finished tile to its epilogue warpgroup: neither may change a single output bit."""
+    lengths, d, H, dff = synth.config("C4-wiki512")
+    T = int(np.sum(lengths))
+    layer = P().EncoderLayer(P().EncoderParams.from_host(synth.encoder_weights(d, H, dff, seed=7)))
+    x = bf16_cuda(synth.activations(T, d))
+    lay = _layout(lengths, H)
+    ref = layer(x, lay).clone()
+    qkv = bf16_cuda(synth.normal((T, 3 * d), 31))
+    o_ref = P().ragged_attention(lay, qkv, d // H).clone()
+    for _ in range(20):
+        assert torch.equal(layer(x, lay), ref)
+        assert torch.equal(P().ragged_attention(lay, qkv, d // H), o_ref)
+
+
 # ---------------------------------------------------------------- layer stack (SURVEY f-4)
 @pytest.mark.parametrize("n_layers,lengths,d,H,dff", [
     (6, [3, 130, 1, 64, 0, 257], 512, 8, 2048),   # the paper's 6-layer model dims (PAPER.md:908-912)
