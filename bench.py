@@ -305,6 +305,10 @@ def main():
     layer = P.EncoderLayer(params)
     layer_launches = layer.launches(T_loc) if T_loc else layer.launches(T_all)  # 5: GEMM + LN fused, else 7
     fused_ln = layer_launches == 5
+    # cora_encoder_forward: batches of <= 256 sequences build the layout in the QKV GEMM's epilogue warps (no
+    # prelude kernel, csrc/api.cu forward_impl); larger batches launch the prelude kernel beside the QKV GEMM
+    prelude_in_gemm = 1 <= len(loc_len) <= 256 and T_loc > 0 and os.environ.get("CORA_QKV_PRELUDE", "1") != "0"
+    prelude_launches = 0 if prelude_in_gemm else 1
     len_dev = torch.tensor(loc_len, dtype=torch.int32, device=dev)
     # every rank holds the whole [T, d] input and output; its own rows are contiguous views of them, so the
     # gather lands in place (no copy)
@@ -680,7 +684,8 @@ def main():
                    "d_ff": dff, "parallelism": f"seq-shard{world}" if world > 1 else "single",
                    "l2": "no flush" if args.no_flush else ("flushed between steps: 256 MB written, then 256 MB read "
                                                             "(the flush's dirty lines leave L2 before the step)"),
-                   "step": f"prelude(a1) + {layer_launches} layer kernels (a2..a8"
+                   "step": ("prelude(a1) in the QKV GEMM's epilogue warps + " if prelude_in_gemm else "prelude(a1) + ")
+                   + f"{layer_launches} layer kernels (a2..a8"
                    + (", LayerNorm fused into the out-proj / FF2 GEMM epilogues)" if fused_ln else ")") + (" per rank; NCCL all-gather timed separately (multi_gpu)" if world > 1 else ""),
                    "launch": "eager" if args.no_graph else "CUDA graph replay per step, programmatic dependent launch"},
         "frac_of_peak": {"burst": value / peaks["bf16_tflops"], "sustained": value / peaks["bf16_tflops_sustained"],
@@ -695,7 +700,7 @@ def main():
         "multi_gpu": gather_info,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (1 + layer_launches) * args.steps,
+        "gpu_launches": (prelude_launches + layer_launches) * args.steps,
         "kernel_timing": ("CUDA events between the kernels in an instrumented replay of the same graph, "
                           f"{args.steps} steps after the timed region; those event nodes disable the PDL overlap, so "
                           "per-kernel times are upper bounds (instrumented step "

@@ -160,8 +160,12 @@ size_t cora_layout_workspace_bytes(int32_t batch, int32_t total_tokens, int32_t 
       .total;
 }
 
-cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
-                                int32_t max_len, void* ws, size_t ws_bytes, cora_layout_t* out, void* stream) {
+}  // extern "C"
+namespace {
+// cora_layout_build without (launch = false) or with the prelude launch: the layout's tables carved from ws
+cora_status_t layout_build_impl(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, void* ws, size_t ws_bytes, cora_layout_t* out, void* stream,
+                                bool launch) {
   if (out == nullptr || !layout_args_ok(batch, total_tokens, heads, max_len)) return CORA_ERR_INVALID;
   if (batch > 0 && lengths == nullptr) return CORA_ERR_INVALID;
   const int64_t ntm = tiles_bound(batch, total_tokens, heads, max_len);
@@ -192,9 +196,17 @@ cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t t
   L.units = reinterpret_cast<int32_t*>(w + c.units);
   L.unit_seq = reinterpret_cast<int32_t*>(w + c.unit_seq);
   L.n_units = reinterpret_cast<int32_t*>(w + c.n_units);
-  const cudaError_t e = launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream));
+  const cudaError_t e =
+      launch ? launch_layout_build(lengths, batch, total_tokens, heads, max_len, L, as_stream(stream)) : cudaSuccess;
   *out = L;
   return e == cudaSuccess ? CORA_OK : CORA_ERR_CUDA;
+}
+}  // namespace
+extern "C" {
+
+cora_status_t cora_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, void* ws, size_t ws_bytes, cora_layout_t* out, void* stream) {
+  return layout_build_impl(lengths, batch, total_tokens, heads, max_len, ws, ws_bytes, out, stream, true);
 }
 
 cora_status_t cora_layout_status(cora_layout_t* layout, void* stream) {
@@ -340,7 +352,8 @@ namespace {
 // cora_encoder_forward), so the QKV GEMM need not wait for that launch before reading x -- it runs under
 // the prelude and waits for it only before completing
 cora_status_t encoder_layer_impl(const cora_encoder_params_t* p, const cora_layout_t* layout, const void* x, void* y,
-                                 void* ws, size_t ws_bytes, void* stream, void* const* events, bool qkv_late_wait) {
+                                 void* ws, size_t ws_bytes, void* stream, void* const* events, bool qkv_late_wait,
+                                 const PreludeArgs* prelude = nullptr) {
   if (p == nullptr || layout == nullptr) return CORA_ERR_INVALID;
   const int32_t d = p->d_model, H = p->heads, ff = p->d_ff, T = layout->total_tokens;
   if (d <= 0 || H <= 0 || ff <= 0 || (d % H) != 0 || (d % 8) != 0 || (ff % 8) != 0 || H != layout->heads)
@@ -379,6 +392,10 @@ cora_status_t encoder_layer_impl(const cora_encoder_params_t* p, const cora_layo
   mark(0);
   GemmArgs g2{x, p->w_qkv, p->b_qkv, nullptr, qkv, T, 3 * d, d, CORA_ACT_NONE};
   g2.late_wait = qkv_late_wait && events == nullptr;
+  if (prelude != nullptr) {  // the QKV GEMM's epilogue warps build the layout (no prelude kernel to wait for)
+    g2.prelude = *prelude;
+    g2.late_wait = false;
+  }
   if ((e = launch_gemm(g2, s)) != cudaSuccess) return cuda_status(e);
   // a3: fused ragged attention
   mark(1);
@@ -434,6 +451,27 @@ cora_status_t cora_encoder_layer_fwd_ex(const cora_encoder_params_t* p, const co
   return encoder_layer_impl(p, layout, x, y, ws, ws_bytes, stream, events, false);
 }
 
+}  // extern "C"
+namespace {
+// Prelude + layer on one layout.  Batches of at most kPreludeInGemmMaxBatch sequences: the QKV GEMM's epilogue
+// warps build the layout while its first units run (no prelude kernel; CORA_QKV_PRELUDE=0 disables), else the
+// prelude kernel runs beside a late-waiting QKV GEMM.
+cora_status_t forward_impl(const cora_encoder_params_t* p, const int32_t* lengths, int32_t batch, int32_t T,
+                           int32_t max_len, void* lay_ws, size_t lay_bytes, const void* x, void* y, void* ws,
+                           size_t ws_bytes, cora_layout_t* L, cora_layout_t* layout_out, void* stream) {
+  const char* pv = getenv("CORA_QKV_PRELUDE");
+  const bool in_gemm = (pv == nullptr || atoi(pv) != 0) && batch >= 1 && batch <= kPreludeInGemmMaxBatch && T > 0;
+  cora_status_t st = layout_build_impl(lengths, batch, T, p->heads, max_len, lay_ws, lay_bytes, L, stream, !in_gemm);
+  if (st != CORA_OK) return st;
+  if (layout_out != nullptr) *layout_out = *L;
+  if (!in_gemm) return encoder_layer_impl(p, L, x, y, ws, ws_bytes, stream, nullptr, true);
+  PreludeArgs pre = prelude_args(lengths, batch, T, p->heads, max_len, *L);
+  pre.nparts = (batch + 3) / 4;  // as the prelude kernel: 4 sequences per part
+  return encoder_layer_impl(p, L, x, y, ws, ws_bytes, stream, nullptr, false, &pre);
+}
+}  // namespace
+extern "C" {
+
 size_t cora_encoder_forward_workspace_bytes(const cora_encoder_params_t* p, int32_t batch, int32_t total_tokens,
                                             int32_t max_len) {
   if (p == nullptr || !layout_args_ok(batch, total_tokens, p->heads, max_len)) return 0;
@@ -450,11 +488,9 @@ cora_status_t cora_encoder_forward(const cora_encoder_params_t* p, const int32_t
   const size_t lay_bytes = cora_layout_workspace_bytes(batch, total_tokens, p->heads, max_len);
   uint8_t* w = static_cast<uint8_t*>(ws);
   cora_layout_t L;
-  cora_status_t st = cora_layout_build(lengths, batch, total_tokens, p->heads, max_len, w, lay_bytes, &L, stream);
-  if (st != CORA_OK) return st;
-  if (layout_out != nullptr) *layout_out = L;
   const size_t off = align_up(lay_bytes);
-  return encoder_layer_impl(p, &L, x, y, w + off, ws_bytes - off, stream, nullptr, true);
+  return forward_impl(p, lengths, batch, total_tokens, max_len, w, lay_bytes, x, y, w + off, ws_bytes - off, &L,
+                      layout_out, stream);
 }
 
 int32_t cora_encoder_layer_launches(const cora_encoder_params_t* p, int32_t total_tokens) {

@@ -64,6 +64,21 @@ constexpr int kAttnHeadDim = 64;  // head_dim of the tcgen05 attention kernel
 #define CORA_PACK_MAX_BATCH 1024
 #endif
 
+// The prelude's inputs and outputs (the layout tables), for the prelude kernels and the QKV GEMM that runs the
+// prelude in its epilogue warps (GemmArgs::prelude)
+struct PreludeArgs {
+  const int32_t* lengths;
+  int32_t batch, total_tokens, heads, max_len;
+  int32_t* row_off;
+  int64_t* attn_off;
+  int32_t *tiles, *tile_seq, *n_tiles, *units, *unit_seq, *n_units, *status, *seq_of_tok, *pos_in_seq;
+  int32_t nparts;  // prelude parts (GEMM: run by CTAs c, c + gridDim, ...); 0 = no prelude
+};
+inline PreludeArgs prelude_args(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
+                                int32_t max_len, const cora_layout_t& L) {
+  return PreludeArgs{lengths, batch, total_tokens, heads, max_len, L.row_off, L.attn_off, L.tiles, L.tile_seq,
+                     L.n_tiles, L.units, L.unit_seq, L.n_units, L.status, L.seq_of_tok, L.pos_in_seq, 0};
+}
 cudaError_t launch_layout_build(const int32_t* lengths, int32_t batch, int32_t total_tokens, int32_t heads,
                                 int32_t max_len, const cora_layout_t& L, cudaStream_t stream);
 
@@ -80,7 +95,11 @@ struct GemmArgs {
   const float* ln_beta = nullptr;
   float ln_eps = 0.f;
   bool late_wait = false;  // a / residual complete before the previous launch: wait for it only at the end
+  // plain GEMM only: the epilogue warps run the prelude (parts c, c + gridDim, ... of prelude.nparts) before
+  // their first unit -- the one-call forward's QKV GEMM (cora_encoder_forward, batch <= kPreludeInGemmMaxBatch)
+  PreludeArgs prelude{};
 };
+constexpr int kPreludeInGemmMaxBatch = 256;
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
 bool gemm_ln_supported(const GemmArgs& g);
 cudaError_t launch_gemm_ln(const GemmArgs& g, cudaStream_t stream);

@@ -36,6 +36,7 @@
 #include <cstdlib>
 
 #include "cora_internal.h"
+#include "prelude_impl.cuh"
 #include "ptx.cuh"
 
 #ifdef CORA_GEMM_TRACE
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
                         const __nv_bfloat16* __restrict__ bias, const float* __restrict__ ln_gamma,
                         const float* __restrict__ ln_beta, float ln_eps, const __nv_bfloat16* __restrict__ res_ptr,
                         __nv_bfloat16* __restrict__ out_ptr, int32_t M, int32_t N, int32_t K, int32_t act,
-                        int32_t late_wait) {
+                        int32_t late_wait, const PreludeArgs pre) {
   // staging buffers per epilogue warp: the residual is TMA-prefetched into one per chunk (RESIDUAL,
   // staged LN), or the row segment lives in registers (LNREG) / there is no residual: one reused buffer
   constexpr int EW = epi_warps<LN, LNREG>();
@@ -636,6 +637,21 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<LN, LNREG>(), 1)
     uint64_t* rbar = res_bar + ew * S::kBufs;
     const uint32_t tmem_empty_lead0 = PAIR ? mapa_shared(&tmem_empty[0], lead_rank) : 0u;
     GW_DECL;
+    if constexpr (EW == 256 / 32 && !RESIDUAL) {
+      if (pre.nparts > 0) {
+        // the prelude (step a1) in the 8 epilogue warps, while the first unit's mainloop runs: its scratch is
+        // the staging buffers (free until the first accumulator), so no extra shared memory and no extra kernel
+        static_assert(sizeof(PreludeSmem<256>) + sizeof(int32_t) * (kPreludeInGemmMaxBatch + 1) <=
+                          static_cast<size_t>(S::kOffBias - S::kOffC), "prelude scratch in the staging buffers");
+        auto& psm = *reinterpret_cast<PreludeSmem<256>*>(smem + S::kOffC);
+        int32_t* s_off = reinterpret_cast<int32_t*>(smem + S::kOffC + sizeof(PreludeSmem<256>));
+        const WarpTeam team{64, 256, 2};
+        for (int part = static_cast<int>(blockIdx.x); part < pre.nparts; part += static_cast<int>(gridDim.x)) {
+          prelude_part<256>(team, psm, s_off, pre, part, pre.nparts);
+          team.sync();  // the scratch is reused by the next part, then by the staging buffers
+        }
+      }
+    }
     int acc = 0;
     uint32_t acc_phase = 0, res_phase = 0;
     for (int u = unit0; u < num_units; u += unit_step) {
@@ -818,7 +834,7 @@ cudaError_t run_gemm(const GemmArgs& g, cudaStream_t stream) {
   return launch_pdl(kern, dim3(grid), dim3(kThreads), S::kAlloc, stream, CL, ta, tb, tc, tr,
                     static_cast<const __nv_bfloat16*>(g.bias), g.ln_gamma, g.ln_beta, g.ln_eps,
                     static_cast<const __nv_bfloat16*>(g.residual), static_cast<__nv_bfloat16*>(g.c), g.m, g.n, g.k,
-                    g.act, g.late_wait ? 1 : 0);
+                    g.act, g.late_wait ? 1 : 0, g.prelude);
 }
 
 }  // namespace

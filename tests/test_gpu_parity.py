@@ -719,7 +719,10 @@ def test_forward_host_graph_replay_and_recapture():
 
 
 # ---------------------------------------------------------------- prelude + layer in one call
-@pytest.mark.parametrize("lengths", [[3, 130, 1, 64], list(synth.config("C3")[0])], ids=lambda l: f"B{len(l)}")
+@pytest.mark.parametrize("lengths", [[3, 130, 1, 64], list(synth.config("C3")[0]), list(synth.config("C4-wiki512")[0]),
+                                     list(synth.config("C2-mnli")[0]), [0, 5, 0, 200, 1] * 51 + [7],
+                                     list(synth.uniform_lengths(300, 0, 200, seed=4))],
+                         ids=lambda l: f"B{len(l)}")
 def test_encoder_forward_equals_layout_plus_layer(lengths):
     d, H, dff = 512, 8, 2048
     w = synth.encoder_weights(d, H, dff)
@@ -729,11 +732,20 @@ def test_encoder_forward_equals_layout_plus_layer(lengths):
     ref = P().encoder_layer(x, _layout(lengths, H), params)
     fwd = P().EncoderForward(params)
     Lt = torch.tensor(np.asarray(lengths, np.int32), device="cuda")
-    for _ in range(2):  # the QKV GEMM overlaps the prelude; the result must not depend on it
+    ref_tb = {k: v.cpu() for k, v in _layout(lengths, H).tables().items()}
+    for _ in range(2):  # the QKV GEMM builds the layout in its epilogue warps (batch <= 256); same bits
         y = fwd(Lt, T, x)
         torch.cuda.synchronize()
         assert fwd.status() == 0
         assert torch.equal(y, ref)
+        lay = object.__new__(P().RaggedLayout)  # a view of the call's layout (layout_out)
+        lay.c, lay.ws = fwd.layout, fwd.ws  # the call's layout lives at the start of its workspace
+        tb = {k: v.cpu() for k, v in lay.tables().items()}
+        n, nu = int(ref_tb["n_tiles"][0]), int(ref_tb["n_units"][0])
+        for k in ("row_off", "attn_off", "seq_of_tok", "pos_in_seq", "n_tiles", "n_units", "status"):
+            assert torch.equal(tb[k], ref_tb[k]), k
+        assert torch.equal(tb["tiles"][:n], ref_tb["tiles"][:n]) and torch.equal(tb["tile_seq"][:2 * n], ref_tb["tile_seq"][:2 * n])
+        assert torch.equal(tb["units"][:nu], ref_tb["units"][:nu]) and torch.equal(tb["unit_seq"][:2 * nu], ref_tb["unit_seq"][:2 * nu])
 
 
 # ---------------------------------------------------------------- the library's NCCL all-gather (one rank)
