@@ -728,11 +728,9 @@ cora_status_t host_forward_enqueue(const cora_encoder_params_t* p, const int32_t
     if (cudaStreamWaitEvent(s, hp->h2d_ev[c], 0) != cudaSuccess) return CORA_ERR_CUDA;
     if (nt > 0) {
       cora_layout_t Lc;
-      cora_status_t st = cora_layout_build(d_len + seq_begin[c], nb, nt, p->heads, max_len, chunk_lay_ws, lay_bytes,
-                                           &Lc, stream);
-      if (st != CORA_OK) return st;
-      st = encoder_layer_impl(p, &Lc, d_x + row * tok_begin[c], d_y + row * tok_begin[c], w, layer_ws, stream, nullptr,
-                              true);
+      const cora_status_t st = forward_impl(p, d_len + seq_begin[c], nb, nt, max_len, chunk_lay_ws, lay_bytes,
+                                            d_x + row * tok_begin[c], d_y + row * tok_begin[c], w, layer_ws, &Lc,
+                                            nullptr, stream);
       if (st != CORA_OK) return st;
     }
     if (cudaEventRecord(hp->comp_ev[c], s) != cudaSuccess) return CORA_ERR_CUDA;
