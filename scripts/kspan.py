@@ -91,14 +91,18 @@ def main():
                 slots = [0] if si == 0 else ([1] if si == 1 else [2, 3, 4, 5])
                 for s in slots:
                     span[s] = a[s]
-            t0 = min(span[s][0] for s in range(6))
+            t0 = min(span[s][0] for s in range(6) if span[s][5] > 0)  # kernels that ran (the prelude may not)
             r = (span[:6, :5] - t0).astype(np.float64) / 1e3
             rows.append(r)
+            ran = [span[s][5] > 0 for s in range(6)]
         med = np.median(np.stack(rows), axis=0)
         print(f"== {cfg}: B={len(lengths)} T={T}  step (events) median {np.median(steps):.1f} us")
         print(f"  {'kernel':<12} {'entry':>7} {'wait0':>7} {'wait1':>7} {'exit':>7} | {'wait1->exit':>11} {'tail':>6}")
         prev_exit = 0.0
         for s in ORDER:
+            if not ran[s]:
+                print(f"  {NAMES[s]:<12} (not launched: inside the QKV GEMM)")
+                continue
             e, w1, w0, x_, xm = med[s][0], med[s][2], med[s][3], med[s][1], med[s][4]
             print(f"  {NAMES[s]:<12} {e:7.1f} {w0:7.1f} {w1:7.1f} {x_:7.1f} | {x_ - w1:11.1f} {x_ - xm:6.1f}")
         sys.stdout.flush()
