@@ -186,9 +186,11 @@ size_t cora_encoder_forward_workspace_bytes(const cora_encoder_params_t* p, int3
                                             int32_t max_len);
 
 /* One ragged batch through one layer from its lengths: cora_layout_build (step a1) + the layer (a2..a8)
- * in one call, with the tables in `ws`.  Because x must be complete before this call, the QKV GEMM does
- * not wait for the prelude (which it does not read): it runs under it and only waits for it before
- * completing, taking the prelude off the critical path.  lengths: device int32 [batch]; x, y as for
+ * in one call, with the tables in `ws` (bitwise the tables cora_layout_build writes).  Batches of at most
+ * 256 sequences: the QKV GEMM's epilogue warps build the tables while its first units' mainloops run (no
+ * prelude kernel).  Larger batches: the prelude kernel runs and, because x must be complete before this
+ * call, the QKV GEMM does not wait for it (it does not read the tables) and only waits before completing.
+ * Either way the prelude is off the critical path.  lengths: device int32 [batch]; x, y as for
  * cora_encoder_layer_fwd; layout_out (may be NULL) receives the layout (for cora_layout_status).
  * Errors as cora_layout_build and cora_encoder_layer_fwd. */
 cora_status_t cora_encoder_forward(const cora_encoder_params_t* p, const int32_t* lengths, int32_t batch,
